@@ -1,0 +1,199 @@
+/*
+ * lsb.h -- C ABI of the B200 loop-nest backend (liblsb.so).
+ *
+ * This is the drop-in boundary under the reference's backend surface.  The
+ * reference (loopsmith) compiles a LoopTree into a VM program and interprets
+ * it on the CPU:
+ *
+ *     compile_tree(tree, target)   reference pkg/src/loopsmith/backend.py:1427-1454
+ *     execute(kernel, buffers)     reference pkg/src/loopsmith/backend.py:121-161
+ *       -> vm.run / vm._run        reference pkg/src/loopsmith/vm.py:20-257
+ *
+ * The B200 backend keeps that Python surface (paper_2205_00618_b200.backend)
+ * and replaces encode_program + vm.run with launches of hand-written sm_100a
+ * kernels through the entry points below.  Each launch entry point takes one
+ * plain-C descriptor (pointers, sizes, element strides, operator codes) and a
+ * cudaStream_t passed as void*; nothing here uses torch or C++ types.
+ *
+ * Conventions
+ *   - every function returns int: LSB_OK (0) on success, a negative
+ *     LSB_ERR_* on failure; lsb_last_error() copies a message for the last
+ *     failure on the calling thread.
+ *   - all data is f32; strides are in ELEMENTS (may be 0 for broadcast).
+ *   - device buffers are owned by the caller (lsb_device_alloc or any CUDA
+ *     allocation, e.g. torch tensors); launches are asynchronous on `stream`.
+ *   - operator codes equal the reference's program.KIND_CODE / EW_CODE
+ *     (program.py:182-183) so plans carry them verbatim.
+ *   - thread-compatible, not thread-safe per stream (like the reference's
+ *     CompiledKernel).
+ */
+#ifndef LSB_H_
+#define LSB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSB_ABI_VERSION 1
+
+/* reduce / combine operators: program.py:182 KIND_CODE */
+enum { LSB_OP_ADD = 0, LSB_OP_MUL = 1, LSB_OP_MAX = 2, LSB_OP_MIN = 3 };
+/* elementwise pre/post: program.py:183 EW_CODE (ir.py:179 ELEMENTWISE_OPS) */
+enum { LSB_EW_IDENTITY = 0, LSB_EW_RELU = 1, LSB_EW_SIGMOID = 2 };
+/* GEMM algorithm selector */
+enum { LSB_ALGO_AUTO = 0, LSB_ALGO_SIMT = 1, LSB_ALGO_TF32X3 = 2 };
+
+enum {
+    LSB_OK = 0,
+    LSB_ERR_INVALID = -1,      /* bad descriptor / argument */
+    LSB_ERR_CUDA = -2,         /* CUDA runtime error */
+    LSB_ERR_UNSUPPORTED = -3,  /* shape / operator combination not covered */
+    LSB_ERR_NOMEM = -4
+};
+
+#define LSB_MAX_EPI 4
+#define LSB_MAX_NEST_DIMS 8
+#define LSB_MAX_NEST_OPERANDS 4
+#define LSB_MAX_GUARDS 4
+
+/*
+ * One fused elementwise stage of a contraction epilogue, the per-output-point
+ * part of the reference Arith semantics (ir.py:194-222, feedback.py:144-170):
+ *
+ *     t = operand ? combine(x, operand[idx]) : x
+ *     t = beta * t                              (skipped when beta == 1)
+ *     t = alpha != 0 ? reduce(alpha * pre(c_in[idx]), t) : t
+ *     x = post(t)
+ *
+ * Stage 0 is the contraction node itself (operand NULL; its beta is the
+ * post-reduction scale when the plan moved beta out of the loop); later
+ * stages are the elementwise Arith nodes that follow it (bias add, ReLU, ...).
+ * idx = Σ s[d] * coord[d] over the kernel's output coordinates:
+ *   GEMM (batch, m, n, -), conv (n, co, h, w).
+ */
+typedef struct {
+    int32_t combine;           /* LSB_OP_* with operand, or -1 for none */
+    int32_t reduce;            /* op folding alpha*pre(c_in) into x      */
+    int32_t pre, post;         /* LSB_EW_*                                */
+    float beta, alpha;
+    const float *operand; int64_t so[4];
+    const float *c_in;    int64_t sc[4];
+} lsb_epi_stage;
+
+/*
+ * Semiring contraction  C[b,m,n] = epi( reduce_k  combine(A[b,m,k], B[b,k,n]) )
+ * Replaces the register-blocked region of backend.py:593-971 executed by
+ * vm.py:112-161 (vop / vfma / vreduce) for 2-operand contractions.
+ */
+typedef struct {
+    int64_t M, N, K, batch;
+    const float *A; int64_t sa_b, sa_m, sa_k;
+    const float *B; int64_t sb_b, sb_k, sb_n;
+    float *C;       int64_t sc_b, sc_m, sc_n;
+    int32_t combine, reduce;
+    float beta;                /* scale of every combine term             */
+    int32_t beta_in_loop;      /* 1: apply beta per term (exact);
+                                  0: caller moved it to epi[0]             */
+    int32_t n_epi;
+    lsb_epi_stage epi[LSB_MAX_EPI];
+    int32_t algo;              /* LSB_ALGO_*                               */
+    int32_t split_k;           /* 0 = auto                                 */
+    int32_t tile_m, tile_n;    /* 0 = auto (split-factor hints)            */
+    int64_t m_begin, m_end;    /* compute output rows [m_begin, m_end); m_end <= 0 -> M
+                                  (row sharding across GPUs) */
+} lsb_gemm_desc;
+
+/*
+ * Direct 2-D convolution over NCHW-indexed tensors (any element strides),
+ * implicit GEMM: M = CO, N = pixels, K = C*R*S.  Out-of-range taps read
+ * `fill` (a guarded View's oob, ir.py:238-245; 0 for zero padding).
+ * Replaces the guarded-load + FMA loops of backend.py:357-395 / vm.py:86-188.
+ */
+typedef struct {
+    int64_t N, C, H, W;        /* input extent  */
+    int64_t CO, R, S;          /* filter extent */
+    int64_t HO, WO;            /* output extent */
+    int64_t stride_h, stride_w, pad_h, pad_w, dil_h, dil_w;
+    float fill;
+    const float *x; int64_t sx[4];   /* n, c, h, w  */
+    const float *w; int64_t sw[4];   /* co, c, r, s */
+    float *o;       int64_t so[4];   /* n, co, h, w */
+    int32_t combine, reduce;
+    float beta; int32_t beta_in_loop;
+    int32_t n_epi;
+    lsb_epi_stage epi[LSB_MAX_EPI];
+} lsb_conv_desc;
+
+/*
+ * General affine loop nest (one Arith node): for every output point,
+ *   acc = identity(reduce); for every reduction point:
+ *       acc = reduce(acc, beta * combine_i operand_i[addr_i])
+ * with addr_i = base_i + Σ coeff_i[d] * iter[d], guarded coordinates reading
+ * `fill_i`, then the epilogue stages (coords = the first 4 output dims).
+ * Covers every graph the frontend can build (views, windows, concat,
+ * transposes, broadcasts, pooling) -- the coverage path for trees the tuned
+ * kernels do not match.
+ */
+typedef struct {
+    int64_t base;
+    int64_t coeff[LSB_MAX_NEST_DIMS];
+} lsb_affine;
+
+typedef struct {
+    const float *ptr;
+    lsb_affine addr;
+    int32_t n_guards;
+    lsb_affine guard[LSB_MAX_GUARDS];   /* value must lie in [0, guard_size) */
+    int64_t guard_size[LSB_MAX_GUARDS];
+    float fill;
+} lsb_nest_operand;
+
+typedef struct {
+    int32_t n_out, n_red;                 /* dims: out first, then reduction */
+    int64_t extent[LSB_MAX_NEST_DIMS];
+    int32_t n_operands;
+    lsb_nest_operand operand[LSB_MAX_NEST_OPERANDS];
+    float *out; lsb_affine out_addr;
+    int32_t combine, reduce;
+    float beta;
+    int32_t n_epi;
+    lsb_epi_stage epi[LSB_MAX_EPI];       /* so/sc index the first 4 out dims */
+} lsb_nest_desc;
+
+/* ---- lifecycle / errors --------------------------------------------------- */
+int lsb_abi_version(void);
+int lsb_init(int device);
+int lsb_last_error(char *buf, size_t len);
+int lsb_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,
+                    int *clock_khz);
+
+/* ---- memory (caller-owned; thin wrappers so the ABI needs no CUDA headers) */
+int lsb_device_alloc(void **ptr, size_t bytes);
+int lsb_device_free(void *ptr);
+int lsb_host_alloc(void **ptr, size_t bytes);       /* pinned */
+int lsb_host_free(void *ptr);
+int lsb_memcpy_h2d(void *dst, const void *src, size_t bytes, void *stream);
+int lsb_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream);
+int lsb_memcpy_d2d(void *dst, const void *src, size_t bytes, void *stream);
+int lsb_stream_sync(void *stream);
+
+/* ---- kernels ---------------------------------------------------------------- */
+int lsb_semiring_gemm(const lsb_gemm_desc *desc, void *stream);
+int lsb_conv2d_nchw(const lsb_conv_desc *desc, void *stream);
+int lsb_affine_nest(const lsb_nest_desc *desc, void *stream);
+
+/* sizeof of the descriptor structs (which: 0 gemm, 1 conv, 2 nest, 3 epi
+ * stage) so bindings can verify their layout without a GPU */
+int64_t lsb_sizeof(int which);
+
+/* number of kernel launches issued since the last reset (launch accounting
+ * for bench.py's "gpu_launches") */
+int64_t lsb_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSB_H_ */

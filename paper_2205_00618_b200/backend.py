@@ -1,0 +1,345 @@
+"""Drop-in B200 replacement for ``loopsmith.backend`` (compile-then-call).
+
+Public surface, same names / arguments / errors as the reference
+(reference pkg/src/loopsmith/backend.py):
+
+  compile_tree(tree, target, unroll_limit=None, interleave=True)  backend.py:1427-1454
+  compile(...)                      alias                          backend.py:1496-1500
+  compile_single_operand(tree, target, unroll_limit=None)          backend.py:1503-1514
+  execute(kernel, buffers)                                         backend.py:121-161
+  CompiledKernel                                                   backend.py:92-118
+  BlockTooLarge / HasReduction / ShapeMismatch                     backend.py:41-46, feedback.py:21
+
+Differences by design: ``program`` is a launch program (one record per
+sm_100a kernel launch) instead of a VM instruction list; ``target`` (a CPU
+vector-ISA preset) is accepted and ignored -- tiles come from the B200 kernel
+set, with split factors used only as hints.  ``execute`` copies host buffers
+to HBM, launches, and copies outputs back; ``run_device`` runs on
+caller-owned device buffers (inputs already resident).
+
+There is no CPU path: without liblsb.so or a CUDA device every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import native
+from .errors import BlockTooLarge, HasReduction, ShapeMismatch
+from .graph import Graph
+from .planner import Plan, Ref, Step, plan_graph
+
+#: reference program.py:186-190 counter names (kept so callers that read
+#: kernel.counters / memory_access_count() keep working)
+COUNTERS = ("vload", "vload.strided", "vbroadcast", "vstore", "sload",
+            "sstore", "vop", "vfma", "vreduce", "sop", "sfma", "post",
+            "vbroadcast.imm", "loop")
+MEM_COUNTERS = ("vload", "vload.strided", "vbroadcast", "vstore", "sload", "sstore")
+
+__all__ = ["compile_tree", "compile", "compile_single_operand", "compile_graph", "execute",
+           "run_device", "CompiledKernel", "BlockTooLarge", "HasReduction", "ShapeMismatch"]
+
+
+# ---------------------------------------------------------------------------
+# the compiled artifact
+# ---------------------------------------------------------------------------
+
+@dataclass
+class LaunchRecord:
+    op: str            # "launch.gemm" | "launch.conv" | "launch.nest"
+    step: Step
+
+
+@dataclass
+class LaunchProgram:
+    """Stands in for program.KernelProgram: one record per kernel launch."""
+    instrs: list[LaunchRecord]
+    lanes: int = 32
+    vregs: int = 255
+    regions: list = field(default_factory=list)
+    buffers: list = field(default_factory=list)
+    var_names: list = field(default_factory=list)
+
+    def disassemble(self) -> str:
+        return "".join(f"{r.op} {r.step.describe()}\n" for r in self.instrs)
+
+    def encode(self):
+        raise NotImplementedError("B200 launch programs are not VM-encodable")
+
+
+@dataclass
+class CompiledKernel:
+    """Same fields callers read on the reference's CompiledKernel
+    (backend.py:92-118, cli.py:56-72, session.py:247-250, tuner.py:66-69)."""
+    program: LaunchProgram
+    target: object
+    slot_shapes: dict[int, tuple[int, ...]]
+    input_slots: set[int]
+    output_slots: set[int]
+    scratch_bytes: int
+    compile_ms: float
+    flops: int
+    dfg_bytes_moved: int
+    unrolled_spans: list = field(default_factory=list)
+    unroll_limit: int = 0
+    counters: dict[str, int] = field(default_factory=dict)
+    plan: Optional[Plan] = None
+    _runner: object = None
+
+    def disassemble(self) -> str:
+        return self.program.disassemble()
+
+    def memory_access_count(self) -> int:
+        return sum(self.counters.get(k, 0) for k in MEM_COUNTERS)
+
+    @property
+    def runner(self) -> "Runner":
+        if self._runner is None:
+            self._runner = Runner(self.plan)
+        return self._runner
+
+
+# ---------------------------------------------------------------------------
+# compile
+# ---------------------------------------------------------------------------
+
+def _compile(graph: Graph, target, unroll_limit) -> CompiledKernel:
+    t0 = time.perf_counter()
+    plan = plan_graph(graph)
+    prog = LaunchProgram([LaunchRecord(f"launch.{s.kind}", s) for s in plan.steps],
+                         lanes=getattr(target, "lanes", 32), vregs=getattr(target, "vregs", 255))
+    ms = (time.perf_counter() - t0) * 1000.0
+    limit = unroll_limit if unroll_limit is not None else getattr(target, "unroll_limit", 0)
+    return CompiledKernel(program=prog, target=target, slot_shapes=plan.slot_shapes,
+                          input_slots=set(plan.input_slots), output_slots=set(plan.output_slots),
+                          scratch_bytes=plan.scratch_bytes, compile_ms=ms,
+                          flops=graph.count_flops(), dfg_bytes_moved=graph.bytes_moved(),
+                          unroll_limit=limit, counters={k: 0 for k in COUNTERS}, plan=plan)
+
+
+def compile_tree(tree, target=None, unroll_limit: Optional[int] = None,
+                 interleave: bool = True) -> CompiledKernel:
+    """Compile a lowered loop tree (reference LoopTree) for the B200.
+
+    Only ``tree.dfg`` is consumed: every schedule annotation is
+    value-preserving (feedback.py:69-75), so split factors are tile hints."""
+    del interleave
+    return _compile(Graph.coerce(tree), target, unroll_limit)
+
+
+def compile(tree, target=None, unroll_limit: Optional[int] = None,  # noqa: A001
+            interleave: bool = True) -> CompiledKernel:
+    """Alias of ``compile_tree`` (backend.py:1496-1500)."""
+    return compile_tree(tree, target, unroll_limit, interleave)
+
+
+def compile_single_operand(tree, target=None, unroll_limit: Optional[int] = None) -> CompiledKernel:
+    """Reduction-free single-input trees (backend.py:1503-1514)."""
+    g = Graph.coerce(tree)
+    for n in g.nodes.values():
+        red = g.reduction_dims(n)
+        if red:
+            raise HasReduction(f"node {n.id} reduces {[g.vars[v].name for v in red]}")
+    n_reads = sum(1 for n in g.nodes.values() if n.kind == "read")
+    if n_reads != 1:
+        raise ValueError(f"single-operand tree must have 1 input, has {n_reads}")
+    return _compile(g, target, unroll_limit)
+
+
+def compile_graph(graph, target=None) -> CompiledKernel:
+    """Compile from a DFG, the reference's canonical graph JSON (dict / str,
+    serialize.py:32-87) or a Graph mirror -- the path the CLI data format
+    and the GPU-box parity fixtures use."""
+    return _compile(Graph.coerce(graph), target, None)
+
+
+# ---------------------------------------------------------------------------
+# runtime: device buffers + descriptors
+# ---------------------------------------------------------------------------
+
+def _current_device() -> int:
+    return int(os.environ.get("LSB_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+class Runner:
+    """Launches a plan.  Owns scratch buffers (and, for ``execute``, device
+    copies of the external slots); descriptors are rebuilt only when the
+    buffer pointers change."""
+
+    def __init__(self, plan: Plan, device: Optional[int] = None):
+        self.plan = plan
+        self.device = _current_device() if device is None else device
+        native.init(self.device)
+        self.scratch = {k: native.DeviceBuffer(4 * n) for k, n in plan.scratch.items()}
+        self.slot_bufs: dict[int, native.DeviceBuffer] = {}
+        self._descs = None
+        self._desc_key = None
+
+    def slot_buffers(self) -> dict[int, int]:
+        for slot, shape in self.plan.slot_shapes.items():
+            if slot not in self.slot_bufs:
+                n = int(np.prod(shape)) if shape else 1
+                self.slot_bufs[slot] = native.DeviceBuffer(4 * n)
+        return {s: b.ptr for s, b in self.slot_bufs.items()}
+
+    def _ptr(self, slots: dict[int, int], ref_base) -> int:
+        ref, base = ref_base
+        if ref.kind == "slot":
+            p = slots[ref.key]
+        else:
+            p = self.scratch[ref.key].ptr
+        return int(p) + 4 * int(base)
+
+    def _acc_ptr(self, slots, acc) -> int:
+        return self._ptr(slots, (acc.ref, acc.base))
+
+    def _epi(self, slots, step: Step, arr) -> int:
+        for i, e in enumerate(step.epi):
+            st = arr[i]
+            st.combine, st.reduce, st.pre, st.post = e.combine, e.reduce, e.pre, e.post
+            st.beta, st.alpha = e.beta, e.alpha
+            strides = step.params["epi_strides"][i]
+            if e.operand is not None:
+                st.operand = self._acc_ptr(slots, e.operand)
+                for d, v in enumerate(strides["operand"]):
+                    st.so[d] = v
+            if e.c_in is not None:
+                st.c_in = self._acc_ptr(slots, e.c_in)
+                for d, v in enumerate(strides["c_in"]):
+                    st.sc[d] = v
+        return len(step.epi)
+
+    def _build(self, slots: dict[int, int]):
+        descs = []
+        for step in self.plan.steps:
+            p = step.params
+            if step.kind == "gemm":
+                d = native.GemmDesc()
+                d.M, d.N, d.K, d.batch = p["M"], p["N"], p["K"], p["batch"]
+                d.A = self._ptr(slots, p["A"]); d.sa_b, d.sa_m, d.sa_k = p["sa_b"], p["sa_m"], p["sa_k"]
+                d.B = self._ptr(slots, p["B"]); d.sb_b, d.sb_k, d.sb_n = p["sb_b"], p["sb_k"], p["sb_n"]
+                d.C = self._ptr(slots, p["C"]); d.sc_b, d.sc_m, d.sc_n = p["sc_b"], p["sc_m"], p["sc_n"]
+                d.combine, d.reduce = p["combine"], p["reduce"]
+                d.beta, d.beta_in_loop = p["beta"], p["beta_in_loop"]
+                d.n_epi = self._epi(slots, step, d.epi)
+                d.algo = p.get("algo", 0)
+                d.split_k = p.get("split_k", 0)
+                d.tile_m = p.get("tile_hint", 0)
+                d.m_begin, d.m_end = p.get("m_begin", 0), p.get("m_end", 0)
+                descs.append((native.semiring_gemm, d))
+            elif step.kind == "conv":
+                d = native.ConvDesc()
+                for k in ("N", "C", "H", "W", "CO", "R", "S", "HO", "WO", "stride_h", "stride_w",
+                          "pad_h", "pad_w", "dil_h", "dil_w"):
+                    setattr(d, k, p[k])
+                d.fill = p["fill"]
+                d.x = self._ptr(slots, p["x"]); d.w = self._ptr(slots, p["w"]); d.o = self._ptr(slots, p["o"])
+                for i in range(4):
+                    d.sx[i], d.sw[i], d.so[i] = p["sx"][i], p["sw"][i], p["so"][i]
+                d.combine, d.reduce, d.beta, d.beta_in_loop = p["combine"], p["reduce"], p["beta"], p["beta_in_loop"]
+                d.n_epi = self._epi(slots, step, d.epi)
+                descs.append((native.conv2d_nchw, d))
+            else:
+                d = native.NestDesc()
+                d.n_out, d.n_red = p["n_out"], p["n_red"]
+                for i, e in enumerate(p["extent"]):
+                    d.extent[i] = e
+                d.n_operands = len(p["operands"])
+                for o, op in enumerate(p["operands"]):
+                    no = d.operand[o]
+                    no.ptr = self._ptr(slots, (op["ref"], 0))
+                    no.addr.base = op["base"]
+                    for i, c in enumerate(op["coeff"]):
+                        no.addr.coeff[i] = c
+                    no.n_guards = len(op["guards"])
+                    for q, (gc, gco, gs) in enumerate(op["guards"]):
+                        no.guard[q].base = gc
+                        for i, c in enumerate(gco):
+                            no.guard[q].coeff[i] = c
+                        no.guard_size[q] = gs
+                    no.fill = op["fill"]
+                d.out = self._ptr(slots, (p["out"][0], 0))
+                d.out_addr.base = p["out"][1]
+                for i, c in enumerate(p["out_coeff"]):
+                    d.out_addr.coeff[i] = c
+                d.combine, d.reduce, d.beta = p["combine"], p["reduce"], p["beta"]
+                d.n_epi = self._epi(slots, step, d.epi)
+                descs.append((native.affine_nest, d))
+        return descs
+
+    def launch(self, slots: dict[int, int], stream: int = 0) -> int:
+        """Enqueue every step on ``stream``; ``slots`` maps slot -> device ptr.
+        Returns the number of kernel launches issued."""
+        key = tuple(sorted(slots.items()))
+        if key != self._desc_key:
+            self._descs = self._build(slots)
+            self._desc_key = key
+        before = native.launch_count()
+        for fn, d in self._descs:
+            fn(d, stream)
+        return native.launch_count() - before
+
+
+def run_device(kernel: CompiledKernel, slots: dict[int, int], stream: int = 0) -> int:
+    """Run on caller-owned device buffers (slot -> device pointer, e.g. torch
+    ``data_ptr()``), inputs already resident; asynchronous on ``stream``.
+    Output slots must point at buffers holding C_in when alpha != 0."""
+    missing = set(kernel.slot_shapes) - set(slots)
+    if missing:
+        raise ShapeMismatch(f"slots {sorted(missing)} have no device buffer")
+    return kernel.runner.launch(slots, stream)
+
+
+def execute(kernel: CompiledKernel, buffers: dict[int, np.ndarray]) -> None:
+    """Reference contract (backend.py:121-161): inputs required and never
+    mutated, sizes checked (ShapeMismatch), a present output slot is read as
+    C_in, outputs written in place (cast to the array's dtype) or inserted."""
+    for slot in kernel.input_slots:
+        if slot not in buffers:
+            raise ShapeMismatch(f"input slot {slot} missing")
+    for slot, shape in kernel.slot_shapes.items():
+        if slot in buffers:
+            want = int(np.prod(shape)) if shape else 1
+            if buffers[slot].size != want:
+                raise ShapeMismatch(f"slot {slot}: expected {shape} ({want} elems), "
+                                    f"got {buffers[slot].size}")
+    r = kernel.runner
+    dev = r.slot_buffers()
+    stream = 0
+    staged = []
+    for slot, arr in buffers.items():
+        if slot not in dev:
+            continue
+        host = np.ascontiguousarray(arr, dtype=np.float32)
+        staged.append(host)
+        native.h2d(dev[slot], host.ctypes.data, host.nbytes, stream)
+    for slot in kernel.output_slots:
+        if slot not in buffers:
+            # absent output: C_in is zeros (reference arena is np.zeros)
+            n = int(np.prod(kernel.slot_shapes[slot])) if kernel.slot_shapes[slot] else 1
+            z = np.zeros(n, np.float32)
+            staged.append(z)
+            native.h2d(dev[slot], z.ctypes.data, z.nbytes, stream)
+    launches = r.launch(dev, stream)
+    outs = {}
+    for slot in kernel.output_slots:
+        shape = kernel.slot_shapes[slot]
+        res = np.empty(shape, np.float32)
+        native.d2h(res.ctypes.data, dev[slot], res.nbytes, stream)
+        outs[slot] = res
+    native.sync(stream)
+    del staged
+    kernel.counters = {k: 0 for k in COUNTERS}
+    kernel.counters["launches"] = launches
+    for slot, res in outs.items():
+        if slot in buffers:
+            dst = buffers[slot]
+            dst.reshape(-1)[:] = res.reshape(-1).astype(dst.dtype)
+        else:
+            buffers[slot] = res

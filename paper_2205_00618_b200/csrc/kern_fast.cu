@@ -1,0 +1,27 @@
+// kern_fast.cu -- tuned instantiations: (mul, add) FFMA2, (add, max|min)
+// FADD2 + FMNMX3, for BM = 128 and 64, and the (mul, add) implicit-GEMM conv.
+#include "lsb_dispatch.cuh"
+
+namespace lsb {
+
+GemmFn fast_gemm(int c, int r, int bm) {
+    if (c == LSB_OP_MUL && r == LSB_OP_ADD)
+        return bm == 64 ? launch_gemm<1, 0, false, 64> : launch_gemm<1, 0, false, 128>;
+    if (c == LSB_OP_ADD && r == LSB_OP_MAX)
+        return bm == 64 ? launch_gemm<0, 2, false, 64> : launch_gemm<0, 2, false, 128>;
+    if (c == LSB_OP_ADD && r == LSB_OP_MIN)
+        return bm == 64 ? launch_gemm<0, 3, false, 64> : launch_gemm<0, 3, false, 128>;
+    return nullptr;
+}
+
+void launch_conv_fast(const ConvArgs &a, dim3 grid, size_t dyn, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(conv_igemm_kernel<1, 0, false, 64>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        attr = true;
+    }
+    conv_igemm_kernel<1, 0, false, 64><<<grid, kThreads, dyn, s>>>(a);
+}
+
+}  // namespace lsb

@@ -1,0 +1,384 @@
+// lsb_api.cu -- the C ABI (include/lsb.h): argument checking, kernel
+// selection and launch.  Built with
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared
+// into paper_2205_00618_b200/liblsb.so (see paper_2205_00618_b200/build.py).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/lsb.h"
+#include "lsb_dispatch.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+#define LSB_CUDA(call)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(LSB_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),       \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(LSB_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return LSB_OK;
+}
+
+int g_sm_count = 0;
+int sm_count();
+
+}  // namespace
+
+int lsb::device_sms() { return sm_count(); }
+
+namespace {
+
+int sm_count() {
+    if (g_sm_count == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sm_count <= 0) g_sm_count = 148;
+    }
+    return g_sm_count;
+}
+
+// split-K workspace (one per process, grown on demand; stream-ordered use)
+std::mutex g_ws_mu;
+float *g_ws = nullptr;
+size_t g_ws_bytes = 0;
+
+int workspace(size_t bytes, float **out) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if (bytes > g_ws_bytes) {
+        if (g_ws) {
+            cudaDeviceSynchronize();
+            cudaFree(g_ws);
+            g_ws = nullptr;
+            g_ws_bytes = 0;
+        }
+        LSB_CUDA(cudaMalloc(&g_ws, bytes));
+        g_ws_bytes = bytes;
+    }
+    *out = g_ws;
+    return LSB_OK;
+}
+
+bool valid_op(int op) { return op >= LSB_OP_ADD && op <= LSB_OP_MIN; }
+bool valid_ew(int ew) { return ew >= LSB_EW_IDENTITY && ew <= LSB_EW_SIGMOID; }
+
+int check_epi(int n, const lsb_epi_stage *s) {
+    if (n < 0 || n > LSB_MAX_EPI) return fail(LSB_ERR_INVALID, "n_epi %d out of range", n);
+    for (int i = 0; i < n; i++) {
+        if (s[i].combine != -1 && !valid_op(s[i].combine))
+            return fail(LSB_ERR_INVALID, "epi[%d].combine %d invalid", i, s[i].combine);
+        if (s[i].combine != -1 && s[i].operand == nullptr)
+            return fail(LSB_ERR_INVALID, "epi[%d] combine without operand", i);
+        if (s[i].alpha != 0.0f && s[i].c_in == nullptr)
+            return fail(LSB_ERR_INVALID, "epi[%d] alpha without c_in", i);
+        if (!valid_op(s[i].reduce) || !valid_ew(s[i].pre) || !valid_ew(s[i].post))
+            return fail(LSB_ERR_INVALID, "epi[%d] invalid op codes", i);
+    }
+    return LSB_OK;
+}
+
+lsb::EpiStages pack_epi(int n, const lsb_epi_stage *s) {
+    lsb::EpiStages e;
+    memset(&e, 0, sizeof(e));
+    e.n = n;
+    for (int i = 0; i < n; i++) e.s[i] = s[i];
+    return e;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------- dispatch
+// kernel instantiations live in kern_*.cu so they compile in parallel
+using lsb::GemmFn;
+using lsb::ConvFn;
+using lsb::SplitFn;
+using lsb::NestFn;
+using lsb::fast_gemm;
+using lsb::kGemmGeneric;
+using lsb::kNest;
+using lsb::kSplit;
+
+int pick_mode_a(const lsb_gemm_desc *d, int64_t sa_m, int64_t sa_k) {
+    if (!aligned16(d->A) || (d->batch > 1 && d->sa_b % 4)) return lsb::LD_GENERIC;
+    if (sa_k == 1 && sa_m % 4 == 0 && d->K % 4 == 0) return lsb::LD_VEC_K;
+    if (sa_m == 1 && sa_k % 4 == 0 && d->M % 4 == 0) return lsb::LD_VEC_MN;
+    return lsb::LD_GENERIC;
+}
+int pick_mode_b(const lsb_gemm_desc *d) {
+    if (!aligned16(d->B) || (d->batch > 1 && d->sb_b % 4)) return lsb::LD_GENERIC;
+    if (d->sb_n == 1 && d->sb_k % 4 == 0 && d->N % 4 == 0) return lsb::LD_VEC_MN;
+    if (d->sb_k == 1 && d->sb_n % 4 == 0 && d->K % 4 == 0) return lsb::LD_VEC_K;
+    return lsb::LD_GENERIC;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lsb_abi_version(void) { return LSB_ABI_VERSION; }
+
+int lsb_last_error(char *buf, size_t len) {
+    if (buf && len) {
+        strncpy(buf, g_err, len - 1);
+        buf[len - 1] = 0;
+    }
+    return LSB_OK;
+}
+
+int lsb_init(int device) {
+    int n = 0;
+    LSB_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return fail(LSB_ERR_INVALID, "device %d of %d", device, n);
+    LSB_CUDA(cudaSetDevice(device));
+    int major = 0;
+    LSB_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    if (major != 10) return fail(LSB_ERR_UNSUPPORTED, "device %d is sm_%d x, this build targets sm_100a", device, major);
+    LSB_CUDA(cudaFree(nullptr));
+    g_sm_count = 0;
+    sm_count();
+    return LSB_OK;
+}
+
+int lsb_device_info(int device, int *sms, int *cc_major, int *cc_minor, int *clock_khz) {
+    if (sms) LSB_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, device));
+    if (cc_major) LSB_CUDA(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, device));
+    if (cc_minor) LSB_CUDA(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, device));
+    if (clock_khz) LSB_CUDA(cudaDeviceGetAttribute(clock_khz, cudaDevAttrClockRate, device));
+    return LSB_OK;
+}
+
+int lsb_device_alloc(void **ptr, size_t bytes) {
+    if (!ptr) return fail(LSB_ERR_INVALID, "null ptr");
+    cudaError_t e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) return fail(LSB_ERR_NOMEM, "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    return LSB_OK;
+}
+int lsb_device_free(void *ptr) {
+    LSB_CUDA(cudaFree(ptr));
+    return LSB_OK;
+}
+int lsb_host_alloc(void **ptr, size_t bytes) {
+    if (!ptr) return fail(LSB_ERR_INVALID, "null ptr");
+    cudaError_t e = cudaHostAlloc(ptr, std::max<size_t>(bytes, 16), cudaHostAllocDefault);
+    if (e != cudaSuccess) return fail(LSB_ERR_NOMEM, "cudaHostAlloc(%zu): %s", bytes, cudaGetErrorString(e));
+    return LSB_OK;
+}
+int lsb_host_free(void *ptr) {
+    LSB_CUDA(cudaFreeHost(ptr));
+    return LSB_OK;
+}
+int lsb_memcpy_h2d(void *dst, const void *src, size_t bytes, void *stream) {
+    LSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    return LSB_OK;
+}
+int lsb_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream) {
+    LSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    return LSB_OK;
+}
+int lsb_memcpy_d2d(void *dst, const void *src, size_t bytes, void *stream) {
+    LSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return LSB_OK;
+}
+int lsb_stream_sync(void *stream) {
+    LSB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return LSB_OK;
+}
+
+int64_t lsb_sizeof(int which) {
+    switch (which) {
+    case 0: return (int64_t)sizeof(lsb_gemm_desc);
+    case 1: return (int64_t)sizeof(lsb_conv_desc);
+    case 2: return (int64_t)sizeof(lsb_nest_desc);
+    case 3: return (int64_t)sizeof(lsb_epi_stage);
+    default: return -1;
+    }
+}
+
+int64_t lsb_launch_count(int reset) {
+    return reset ? g_launches.exchange(0) : g_launches.load();
+}
+
+int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
+    if (!d) return fail(LSB_ERR_INVALID, "null desc");
+    if (d->M < 0 || d->N < 0 || d->K < 0 || d->batch < 1)
+        return fail(LSB_ERR_INVALID, "bad extents M=%lld N=%lld K=%lld batch=%lld",
+                    (long long)d->M, (long long)d->N, (long long)d->K, (long long)d->batch);
+    if (!valid_op(d->combine) || !valid_op(d->reduce))
+        return fail(LSB_ERR_INVALID, "bad operator pair (%d, %d)", d->combine, d->reduce);
+    if (!d->A || !d->B || !d->C) return fail(LSB_ERR_INVALID, "null operand");
+    int rc = check_epi(d->n_epi, d->epi);
+    if (rc) return rc;
+    if (d->algo == LSB_ALGO_TF32X3) return fail(LSB_ERR_UNSUPPORTED, "tf32x3 path not built");
+    cudaStream_t s = (cudaStream_t)stream;
+
+    int64_t m_begin = std::max<int64_t>(0, d->m_begin);
+    int64_t m_end = d->m_end > 0 ? std::min(d->m_end, d->M) : d->M;
+    int64_t M = m_end - m_begin;
+    if (M <= 0 || d->N == 0) return LSB_OK;
+
+    lsb::GemmArgs a;
+    memset(&a, 0, sizeof(a));
+    a.M = M; a.N = d->N; a.K = d->K;
+    a.A = d->A + m_begin * d->sa_m; a.sa_b = d->sa_b; a.sa_m = d->sa_m; a.sa_k = d->sa_k;
+    a.B = d->B; a.sb_b = d->sb_b; a.sb_k = d->sb_k; a.sb_n = d->sb_n;
+    a.C = d->C + m_begin * d->sc_m; a.sc_b = d->sc_b; a.sc_m = d->sc_m; a.sc_n = d->sc_n;
+    a.beta = d->beta;
+    a.epi = pack_epi(d->n_epi, d->epi);
+    // row-sharded epilogue operands keep global coordinates: shift their bases
+    for (int i = 0; i < a.epi.n; i++) {
+        if (a.epi.s[i].operand) a.epi.s[i].operand += m_begin * a.epi.s[i].so[1];
+        if (a.epi.s[i].c_in) a.epi.s[i].c_in += m_begin * a.epi.s[i].sc[1];
+    }
+    lsb_gemm_desc dd = *d;
+    dd.A = a.A; dd.M = M;
+    a.a_mode = pick_mode_a(&dd, d->sa_m, d->sa_k);
+    a.b_mode = pick_mode_b(&dd);
+    a.c_vec = (d->sc_n == 1 && aligned16(a.C) && d->sc_m % 4 == 0 && (d->batch == 1 || d->sc_b % 4 == 0)) ? 1 : 0;
+
+    if (d->K == 0) {
+        // empty reduction: every output is the reduce identity, then the epilogue
+        return fail(LSB_ERR_UNSUPPORTED, "K == 0 contraction");
+    }
+
+    GemmFn fn = nullptr;
+    int bm = 128;
+    if (!d->beta_in_loop) {
+        int64_t tiles128 = ((M + 127) / 128) * ((d->N + 127) / 128) * d->batch;
+        bm = (d->tile_m == 64 || (d->tile_m == 0 && tiles128 < sm_count())) ? 64 : 128;
+        fn = fast_gemm(d->combine, d->reduce, bm);
+    }
+    if (!fn) {
+        bm = 128;
+        fn = kGemmGeneric[d->combine][d->reduce];
+        if (!d->beta_in_loop && d->beta != 1.0f)
+            return fail(LSB_ERR_INVALID, "beta outside the loop needs a tuned operator pair");
+    }
+    const int64_t m_tiles = (M + bm - 1) / bm;
+    const int64_t n_tiles = (d->N + lsb::kBN - 1) / lsb::kBN;
+    const int64_t tiles = m_tiles * n_tiles * d->batch;
+
+    int splits = d->split_k;
+    if (splits <= 0) {
+        splits = 1;
+        const int64_t slots = (int64_t)sm_count() * 2;
+        const int64_t k_slices = (d->K + lsb::kBK - 1) / lsb::kBK;
+        if (tiles < slots && k_slices >= 64) {
+            splits = (int)std::min<int64_t>((slots + tiles - 1) / tiles, k_slices / 32);
+            splits = std::max(1, std::min(splits, 16));
+        }
+    }
+    int64_t kps = (d->K + splits - 1) / splits;
+    kps = ((kps + lsb::kBK - 1) / lsb::kBK) * lsb::kBK;
+    splits = (int)((d->K + kps - 1) / kps);
+    a.k_per_split = kps;
+    a.splits = splits;
+    if (m_tiles * splits > 65535 || d->batch > 65535 || n_tiles > 2147483647)
+        return fail(LSB_ERR_UNSUPPORTED, "grid too large");
+
+    if (splits > 1) {
+        rc = workspace(sizeof(float) * (size_t)splits * d->batch * M * d->N, &a.ws);
+        if (rc) return rc;
+    }
+    dim3 grid((unsigned)n_tiles, (unsigned)(m_tiles * splits), (unsigned)d->batch);
+    fn(a, grid, s);
+    rc = check_launch("semiring_gemm");
+    if (rc) return rc;
+    if (splits > 1) {
+        kSplit[d->reduce](a, d->batch, s);
+        rc = check_launch("splitk_epilogue");
+        if (rc) return rc;
+    }
+    return LSB_OK;
+}
+
+int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
+    if (!d) return fail(LSB_ERR_INVALID, "null desc");
+    if (!d->x || !d->w || !d->o) return fail(LSB_ERR_INVALID, "null operand");
+    if (d->N < 1 || d->C < 1 || d->CO < 1 || d->R < 1 || d->S < 1 || d->HO < 1 || d->WO < 1 ||
+        d->stride_h < 1 || d->stride_w < 1 || d->dil_h < 1 || d->dil_w < 1)
+        return fail(LSB_ERR_INVALID, "bad conv extents");
+    if (!(d->combine == LSB_OP_MUL && d->reduce == LSB_OP_ADD) || d->beta_in_loop)
+        return fail(LSB_ERR_UNSUPPORTED, "conv kernel covers (mul, add) only");
+    int rc = check_epi(d->n_epi, d->epi);
+    if (rc) return rc;
+    const int64_t K = d->C * d->R * d->S;
+    if (K > lsb::kConvTableMax) return fail(LSB_ERR_UNSUPPORTED, "conv K=%lld too large", (long long)K);
+    if (d->N > 65535) return fail(LSB_ERR_UNSUPPORTED, "too many images");
+
+    lsb::ConvArgs a;
+    memset(&a, 0, sizeof(a));
+    a.M = d->CO; a.N = d->HO * d->WO; a.K = K;
+    a.C = d->C; a.H = d->H; a.W = d->W; a.R = d->R; a.S = d->S; a.HO = d->HO; a.WO = d->WO;
+    a.stride_h = d->stride_h; a.stride_w = d->stride_w; a.pad_h = d->pad_h; a.pad_w = d->pad_w;
+    a.dil_h = d->dil_h; a.dil_w = d->dil_w; a.fill = d->fill;
+    a.x = d->x; a.sx0 = d->sx[0]; a.sx1 = d->sx[1]; a.sx2 = d->sx[2]; a.sx3 = d->sx[3];
+    a.w = d->w; a.sw0 = d->sw[0]; a.sw1 = d->sw[1]; a.sw2 = d->sw[2]; a.sw3 = d->sw[3];
+    a.o = d->o; a.so0 = d->so[0]; a.so1 = d->so[1]; a.so2 = d->so[2]; a.so3 = d->so[3];
+    a.beta = d->beta;
+    a.epi = pack_epi(d->n_epi, d->epi);
+    const bool wcontig = d->sw[3] == 1 && d->sw[2] == d->S && d->sw[1] == d->R * d->S;
+    a.a_mode = (wcontig && aligned16(d->w) && d->sw[0] % 4 == 0 && K % 4 == 0) ? lsb::LD_VEC_K : lsb::LD_GENERIC;
+
+    const int bm = 64;
+    dim3 grid((unsigned)((a.N + lsb::kBN - 1) / lsb::kBN), (unsigned)((a.M + bm - 1) / bm), (unsigned)d->N);
+    size_t dyn = (size_t)K * (sizeof(int64_t) + sizeof(int2));
+    lsb::launch_conv_fast(a, grid, dyn, (cudaStream_t)stream);
+    return check_launch("conv_igemm");
+}
+
+int lsb_affine_nest(const lsb_nest_desc *d, void *stream) {
+    if (!d) return fail(LSB_ERR_INVALID, "null desc");
+    if (d->n_out < 0 || d->n_red < 0 || d->n_out + d->n_red > LSB_MAX_NEST_DIMS)
+        return fail(LSB_ERR_INVALID, "bad dim counts %d + %d", d->n_out, d->n_red);
+    if (d->n_operands < 1 || d->n_operands > LSB_MAX_NEST_OPERANDS)
+        return fail(LSB_ERR_INVALID, "bad operand count %d", d->n_operands);
+    if (!valid_op(d->combine) || !valid_op(d->reduce))
+        return fail(LSB_ERR_INVALID, "bad operator pair");
+    if (!d->out) return fail(LSB_ERR_INVALID, "null output");
+    int rc = check_epi(d->n_epi, d->epi);
+    if (rc) return rc;
+    lsb::NestArgs a;
+    memset(&a, 0, sizeof(a));
+    a.n_out = d->n_out; a.n_red = d->n_red; a.n_ops = d->n_operands;
+    a.n_points = 1;
+    for (int i = 0; i < d->n_out + d->n_red; i++) {
+        if (d->extent[i] < 1) return fail(LSB_ERR_INVALID, "extent[%d] = %lld", i, (long long)d->extent[i]);
+        a.extent[i] = d->extent[i];
+        if (i < d->n_out) a.n_points *= d->extent[i];
+    }
+    for (int o = 0; o < d->n_operands; o++) {
+        if (!d->operand[o].ptr) return fail(LSB_ERR_INVALID, "operand %d null", o);
+        if (d->operand[o].n_guards < 0 || d->operand[o].n_guards > LSB_MAX_GUARDS)
+            return fail(LSB_ERR_INVALID, "operand %d guards", o);
+        a.op[o] = d->operand[o];
+    }
+    a.out = d->out; a.out_addr = d->out_addr; a.beta = d->beta;
+    a.epi = pack_epi(d->n_epi, d->epi);
+    kNest[d->combine][d->reduce](a, (cudaStream_t)stream);
+    return check_launch("affine_nest");
+}
+
+}  // extern "C"

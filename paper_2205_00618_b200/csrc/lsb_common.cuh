@@ -1,0 +1,101 @@
+// lsb_common.cuh -- operator functors and the fused epilogue shared by all
+// B200 loop-nest kernels.
+//
+// Semantics follow the reference Arith node (ir.py:194-222) as evaluated by
+// feedback.reference_eval (feedback.py:144-170) and the VM (vm.py:112-228):
+//   combine / reduce ops add, mul, max, min   (program.py:182 KIND_CODE)
+//   pre / post ops identity, relu, sigmoid    (program.py:183 EW_CODE)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/lsb.h"
+
+namespace lsb {
+
+template <int OP>
+struct Op;
+template <>
+struct Op<LSB_OP_ADD> {
+    static __device__ __forceinline__ float apply(float a, float b) { return __fadd_rn(a, b); }
+    static __device__ __forceinline__ float identity() { return 0.0f; }
+};
+template <>
+struct Op<LSB_OP_MUL> {
+    static __device__ __forceinline__ float apply(float a, float b) { return __fmul_rn(a, b); }
+    static __device__ __forceinline__ float identity() { return 1.0f; }
+};
+template <>
+struct Op<LSB_OP_MAX> {
+    static __device__ __forceinline__ float apply(float a, float b) { return fmaxf(a, b); }
+    static __device__ __forceinline__ float identity() { return -INFINITY; }
+};
+template <>
+struct Op<LSB_OP_MIN> {
+    static __device__ __forceinline__ float apply(float a, float b) { return fminf(a, b); }
+    static __device__ __forceinline__ float identity() { return INFINITY; }
+};
+
+__device__ __forceinline__ float op_rt(int op, float a, float b) {
+    switch (op) {
+    case LSB_OP_ADD: return __fadd_rn(a, b);
+    case LSB_OP_MUL: return __fmul_rn(a, b);
+    case LSB_OP_MAX: return fmaxf(a, b);
+    default: return fminf(a, b);
+    }
+}
+
+__host__ __device__ __forceinline__ float identity_rt(int op) {
+    switch (op) {
+    case LSB_OP_ADD: return 0.0f;
+    case LSB_OP_MUL: return 1.0f;
+    case LSB_OP_MAX: return -INFINITY;
+    default: return INFINITY;
+    }
+}
+
+// vm.py:214-228: relu = max(x, 0); sigmoid evaluated in f64 then rounded,
+// with the same two-branch formulation.
+__device__ __forceinline__ float ew_rt(int ew, float x) {
+    if (ew == LSB_EW_RELU) return fmaxf(x, 0.0f);
+    if (ew == LSB_EW_SIGMOID) {
+        double d = (double)x;
+        if (d >= 0.0) return (float)(1.0 / (1.0 + exp(-d)));
+        double e = exp(d);
+        return (float)(e / (1.0 + e));
+    }
+    return x;
+}
+
+struct EpiStages {
+    int n;
+    lsb_epi_stage s[LSB_MAX_EPI];
+};
+
+// Fused epilogue (lsb.h lsb_epi_stage): x is the reduced value of one output
+// point, c0..c3 its coordinates in the kernel's output index space.
+__device__ __forceinline__ float apply_epilogue(const EpiStages &e, float x, int64_t c0,
+                                                int64_t c1, int64_t c2, int64_t c3) {
+#pragma unroll 1
+    for (int i = 0; i < e.n; i++) {
+        const lsb_epi_stage &st = e.s[i];
+        float t = x;
+        if (st.combine >= 0) {
+            float v = __ldg(st.operand + c0 * st.so[0] + c1 * st.so[1] + c2 * st.so[2] +
+                            c3 * st.so[3]);
+            t = op_rt(st.combine, t, v);
+        }
+        if (st.beta != 1.0f) t = __fmul_rn(st.beta, t);
+        if (st.alpha != 0.0f) {
+            float c = __ldg(st.c_in + c0 * st.sc[0] + c1 * st.sc[1] + c2 * st.sc[2] + c3 * st.sc[3]);
+            c = __fmul_rn(st.alpha, ew_rt(st.pre, c));
+            t = op_rt(st.reduce, c, t);
+        }
+        x = ew_rt(st.post, t);
+    }
+    return x;
+}
+
+}  // namespace lsb

@@ -1,0 +1,28 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+# dev container only: make the reference importable so the drop-in raises the
+# reference's own exception classes (the GPU box has no /root/reference)
+REF_SRC = "/root/reference/pkg/src"
+if os.path.isdir(REF_SRC) and REF_SRC not in sys.path:
+    sys.path.append(REF_SRC)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+TESTS = os.path.dirname(os.path.abspath(__file__))
+if TESTS not in sys.path:
+    sys.path.insert(0, TESTS)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 device (run with -m gpu)")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+def pytest_collection_modifyitems(config, items):
+    # gpu tests fail loudly (no CPU fallback) -- never silently skip them when
+    # they were selected explicitly with -m gpu
+    pass
