@@ -329,8 +329,13 @@ def execute(kernel: CompiledKernel, buffers: dict[int, np.ndarray]) -> None:
     launches = r.launch(dev, stream)
     outs = {}
     for slot in kernel.output_slots:
-        shape = kernel.slot_shapes[slot]
-        res = np.empty(shape, np.float32)
+        dst = buffers.get(slot)
+        if (dst is not None and dst.dtype == np.float32 and dst.flags.c_contiguous
+                and dst.flags.writeable):
+            # straight into the caller's array (pinned arrays get full DMA speed)
+            native.d2h(dst.ctypes.data, dev[slot], dst.nbytes, stream)
+            continue
+        res = np.empty(kernel.slot_shapes[slot], np.float32)
         native.d2h(res.ctypes.data, dev[slot], res.nbytes, stream)
         outs[slot] = res
     native.sync(stream)

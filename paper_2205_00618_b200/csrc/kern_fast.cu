@@ -4,9 +4,12 @@
 
 namespace lsb {
 
-GemmFn fast_gemm(int c, int r, int bm) {
-    if (c == LSB_OP_MUL && r == LSB_OP_ADD)
+GemmFn fast_gemm(int c, int r, int bm, bool two_level) {
+    if (c == LSB_OP_MUL && r == LSB_OP_ADD) {
+        if (two_level)
+            return bm == 64 ? launch_gemm<1, 0, false, 64, true> : launch_gemm<1, 0, false, 128, true>;
         return bm == 64 ? launch_gemm<1, 0, false, 64> : launch_gemm<1, 0, false, 128>;
+    }
     if (c == LSB_OP_ADD && r == LSB_OP_MAX)
         return bm == 64 ? launch_gemm<0, 2, false, 64> : launch_gemm<0, 2, false, 128>;
     if (c == LSB_OP_ADD && r == LSB_OP_MIN)

@@ -268,7 +268,9 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     if (!d->beta_in_loop) {
         int64_t tiles128 = ((M + 127) / 128) * ((d->N + 127) / 128) * d->batch;
         bm = (d->tile_m == 64 || (d->tile_m == 0 && tiles128 < sm_count())) ? 64 : 128;
-        fn = fast_gemm(d->combine, d->reduce, bm);
+        // two-level accumulation for long fp32 sums (K split into 256-chunks)
+        const bool two = d->reduce == LSB_OP_ADD && d->K > 1024;
+        fn = fast_gemm(d->combine, d->reduce, bm, two);
     }
     if (!fn) {
         bm = 128;

@@ -14,15 +14,15 @@ using NestFn = void (*)(const NestArgs &, cudaStream_t);
 
 int device_sms();                               // lsb_api.cu
 
-GemmFn fast_gemm(int combine, int reduce, int bm);   // kern_fast.cu (nullptr if untuned)
+GemmFn fast_gemm(int combine, int reduce, int bm, bool two_level);   // kern_fast.cu (nullptr if untuned)
 void launch_conv_fast(const ConvArgs &a, dim3 grid, size_t dyn, cudaStream_t s);
 extern const GemmFn kGemmGeneric[4][4];          // kern_generic.cu
 extern const SplitFn kSplit[4];                  // kern_generic.cu
 extern const NestFn kNest[4][4];                 // kern_nest.cu
 
-template <int C, int R, bool B, int BM>
+template <int C, int R, bool B, int BM, bool TWO = false>
 void launch_gemm(const GemmArgs &a, dim3 grid, cudaStream_t s) {
-    semiring_gemm_kernel<C, R, B, BM><<<grid, kThreads, 0, s>>>(a);
+    semiring_gemm_kernel<C, R, B, BM, TWO><<<grid, kThreads, 0, s>>>(a);
 }
 
 }  // namespace lsb

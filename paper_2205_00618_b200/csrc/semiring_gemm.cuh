@@ -28,6 +28,7 @@ namespace lsb {
 constexpr int kBN = 128;
 constexpr int kBK = 8;
 constexpr int kThreads = 256;
+constexpr int kChunkSlices = 32;   // two-level accumulation: fold every 32*BK = 256 k
 #ifndef LSB_MINB128
 #define LSB_MINB128 1   // CTAs per SM for the 128-row tile (register budget)
 #endif
@@ -281,17 +282,38 @@ struct ConvLoader {
 // the register-blocked micro-kernel
 // ---------------------------------------------------------------------------
 
-template <int OPC, int OPR, bool BETA, int TM>
+template <int OPC, int OPR, bool BETA, int TM, bool TWO = false>
 struct Micro {
     // acc[i][jp] holds outputs (row i, cols 2jp, 2jp+1) of the thread's TM x 8 block
     float2 acc[TM][4];
+    // TWO-level accumulation (fp32 sums over long K): acc holds one K chunk,
+    // tot the sum of finished chunks -- keeps the rounding error of K = 16384
+    // sums inside the reference tolerance (SURVEY finding 5)
+    float2 tot[TM][4];
 
     __device__ __forceinline__ void init() {
         const float id = Op<OPR>::identity();
 #pragma unroll
         for (int i = 0; i < TM; i++)
 #pragma unroll
-            for (int j = 0; j < 4; j++) acc[i][j] = make_float2(id, id);
+            for (int j = 0; j < 4; j++) {
+                acc[i][j] = make_float2(id, id);
+                if constexpr (TWO) tot[i][j] = make_float2(id, id);
+            }
+    }
+
+    __device__ __forceinline__ void fold() {
+        if constexpr (TWO) {
+            const float id = Op<OPR>::identity();
+#pragma unroll
+            for (int i = 0; i < TM; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    tot[i][j].x = Op<OPR>::apply(tot[i][j].x, acc[i][j].x);
+                    tot[i][j].y = Op<OPR>::apply(tot[i][j].y, acc[i][j].y);
+                    acc[i][j] = make_float2(id, id);
+                }
+        }
     }
 
     __device__ __forceinline__ void frag(const float *As_k, const float *Bs_k, int ty, int tx,
@@ -374,6 +396,7 @@ struct Micro {
     }
 
     __device__ __forceinline__ float get(int i, int j) const {
+        if constexpr (TWO) return (j & 1) ? tot[i][j >> 1].y : tot[i][j >> 1].x;
         return (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
     }
 };
@@ -388,7 +411,7 @@ __device__ __forceinline__ int col_of(int tx, int j) { return (j < 4 ? 0 : 64) +
 // grid: x = n tiles, y = m tiles * splits, z = batch
 // ---------------------------------------------------------------------------
 
-template <int OPC, int OPR, bool BETA, int BM>
+template <int OPC, int OPR, bool BETA, int BM, bool TWO = false>
 __global__ void __launch_bounds__(kThreads, BM == 128 ? LSB_MINB128 : 2) semiring_gemm_kernel(const GemmArgs p) {
     constexpr int TM = BM / 16;
     __shared__ __align__(16) float As[2][kBK][BM + 4];
@@ -403,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, BM == 128 ? LSB_MINB128 : 2) semirin
     const int64_t kbeg = split * p.k_per_split;
     const int64_t kend = min(p.K, kbeg + p.k_per_split);
 
-    Micro<OPC, OPR, BETA, TM> mk;
+    Micro<OPC, OPR, BETA, TM, TWO> mk;
     mk.init();
     GemmLoader<BM> ld;
 
@@ -412,16 +435,24 @@ __global__ void __launch_bounds__(kThreads, BM == 128 ? LSB_MINB128 : 2) semirin
         ld.store(p, As[0], Bs[0]);
         __syncthreads();
         int buf = 0;
+        int chunk = 0;
         for (int64_t k0 = kbeg; k0 < kend; k0 += kBK) {
             const bool more = k0 + kBK < kend;
             if (more) ld.load(p, bz, m0, n0, k0 + kBK, kend);
             const int kcount = (int)min((int64_t)kBK, kend - k0);
             mk.template slice<BM>(As[buf], Bs[buf], kcount, ty, tx, p.beta);
+            if constexpr (TWO) {
+                if (++chunk == kChunkSlices) {
+                    mk.fold();
+                    chunk = 0;
+                }
+            }
             if (more) ld.store(p, As[buf ^ 1], Bs[buf ^ 1]);
             __syncthreads();
             buf ^= 1;
         }
     }
+    mk.fold();
 
     // ---- epilogue
     if (p.ws != nullptr) {
