@@ -100,11 +100,16 @@ int check_epi(int n, const lsb_epi_stage *s) {
     return LSB_OK;
 }
 
+// stages that leave x unchanged (no operand, beta 1, alpha 0, identity post)
+// are dropped so plain contractions take the epilogue-free store path
 lsb::EpiStages pack_epi(int n, const lsb_epi_stage *s) {
     lsb::EpiStages e;
     memset(&e, 0, sizeof(e));
-    e.n = n;
-    for (int i = 0; i < n; i++) e.s[i] = s[i];
+    for (int i = 0; i < n; i++) {
+        const bool noop = s[i].combine < 0 && s[i].beta == 1.0f && s[i].alpha == 0.0f &&
+                          s[i].post == LSB_EW_IDENTITY;
+        if (!noop) e.s[e.n++] = s[i];
+    }
     return e;
 }
 
@@ -266,8 +271,8 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     GemmFn fn = nullptr;
     int bm = 128;
     if (!d->beta_in_loop) {
-        int64_t tiles128 = ((M + 127) / 128) * ((d->N + 127) / 128) * d->batch;
-        bm = (d->tile_m == 64 || (d->tile_m == 0 && tiles128 < sm_count())) ? 64 : 128;
+        // 64-row tiles only when the rows would leave half a 128-row tile idle
+        bm = (d->tile_m == 64 || (d->tile_m == 0 && M <= 64)) ? 64 : 128;
         // two-level accumulation for long fp32 sums (K split into 256-chunks)
         const bool two = d->reduce == LSB_OP_ADD && d->K > 1024;
         fn = fast_gemm(d->combine, d->reduce, bm, two);
@@ -287,9 +292,16 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
         splits = 1;
         const int64_t slots = (int64_t)sm_count() * 2;
         const int64_t k_slices = (d->K + lsb::kBK - 1) / lsb::kBK;
-        if (tiles < slots && k_slices >= 64) {
-            splits = (int)std::min<int64_t>((slots + tiles - 1) / tiles, k_slices / 32);
-            splits = std::max(1, std::min(splits, 16));
+        // split K when the tiles alone underfill the 2-CTA/SM slots: pick the
+        // split count minimising (waves / splits) + 0.05 * splits, the last term
+        // standing for the partial-sum traffic of the fold kernel
+        if (tiles < slots && k_slices >= 8) {
+            double best = 1e30;
+            for (int s = 1; s <= 16 && s <= k_slices / 2; s++) {
+                const int64_t waves = (tiles * s + slots - 1) / slots;
+                const double cost = (double)waves / s + 0.05 * s;
+                if (cost < best - 1e-9) { best = cost; splits = s; }
+            }
         }
     }
     int64_t kps = (d->K + splits - 1) / splits;

@@ -22,7 +22,14 @@ extern const NestFn kNest[4][4];                 // kern_nest.cu
 
 template <int C, int R, bool B, int BM, bool TWO = false>
 void launch_gemm(const GemmArgs &a, dim3 grid, cudaStream_t s) {
-    semiring_gemm_kernel<C, R, B, BM, TWO><<<grid, kThreads, 0, s>>>(a);
+    constexpr size_t dyn = gemm_dyn_smem<BM>();
+    static bool attr = false;   // > 48 KiB dynamic smem needs an opt-in, once per kernel
+    if (!attr) {
+        cudaFuncSetAttribute(semiring_gemm_kernel<C, R, B, BM, TWO>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        attr = true;
+    }
+    semiring_gemm_kernel<C, R, B, BM, TWO><<<grid, kThreads, dyn, s>>>(a);
 }
 
 }  // namespace lsb

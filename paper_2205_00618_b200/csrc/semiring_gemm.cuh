@@ -29,9 +29,6 @@ constexpr int kBN = 128;
 constexpr int kBK = 8;
 constexpr int kThreads = 256;
 constexpr int kChunkSlices = 32;   // two-level accumulation: fold every 32*BK = 256 k
-#ifndef LSB_MINB128
-#define LSB_MINB128 1   // CTAs per SM for the 128-row tile (register budget)
-#endif
 
 // ---------------------------------------------------------------------------
 // problem descriptors as seen by the device
@@ -278,75 +275,62 @@ struct ConvLoader {
     }
 };
 
-// ---------------------------------------------------------------------------
 // the register-blocked micro-kernel
 // ---------------------------------------------------------------------------
 
-template <int OPC, int OPR, bool BETA, int TM, bool TWO = false>
+template <int TM>
+struct Frag {
+    float a[TM];
+    float b[8];
+};
+
+template <int OPC, int OPR, bool BETA, int TM>
 struct Micro {
     // acc[i][jp] holds outputs (row i, cols 2jp, 2jp+1) of the thread's TM x 8 block
     float2 acc[TM][4];
-    // TWO-level accumulation (fp32 sums over long K): acc holds one K chunk,
-    // tot the sum of finished chunks -- keeps the rounding error of K = 16384
-    // sums inside the reference tolerance (SURVEY finding 5)
-    float2 tot[TM][4];
+
+    static constexpr bool kFFMA2 = OPC == LSB_OP_MUL && OPR == LSB_OP_ADD && !BETA;
+    static constexpr bool kMAX3 = OPC == LSB_OP_ADD && (OPR == LSB_OP_MAX || OPR == LSB_OP_MIN) && !BETA;
 
     __device__ __forceinline__ void init() {
         const float id = Op<OPR>::identity();
 #pragma unroll
         for (int i = 0; i < TM; i++)
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                acc[i][j] = make_float2(id, id);
-                if constexpr (TWO) tot[i][j] = make_float2(id, id);
-            }
+            for (int j = 0; j < 4; j++) acc[i][j] = make_float2(id, id);
     }
 
-    __device__ __forceinline__ void fold() {
-        if constexpr (TWO) {
-            const float id = Op<OPR>::identity();
-#pragma unroll
-            for (int i = 0; i < TM; i++)
-#pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    tot[i][j].x = Op<OPR>::apply(tot[i][j].x, acc[i][j].x);
-                    tot[i][j].y = Op<OPR>::apply(tot[i][j].y, acc[i][j].y);
-                    acc[i][j] = make_float2(id, id);
-                }
-        }
-    }
-
-    __device__ __forceinline__ void frag(const float *As_k, const float *Bs_k, int ty, int tx,
-                                         float (&a)[TM], float (&b)[8]) {
+    __device__ __forceinline__ static void frag(const float *As_k, const float *Bs_k, int ty, int tx,
+                                                Frag<TM> &f) {
         float4 a0 = *reinterpret_cast<const float4 *>(As_k + ty * 4);
-        a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+        f.a[0] = a0.x; f.a[1] = a0.y; f.a[2] = a0.z; f.a[3] = a0.w;
         if constexpr (TM == 8) {
             float4 a1 = *reinterpret_cast<const float4 *>(As_k + 64 + ty * 4);
-            a[TM - 4] = a1.x; a[TM - 3] = a1.y; a[TM - 2] = a1.z; a[TM - 1] = a1.w;
+            f.a[4] = a1.x; f.a[5] = a1.y; f.a[6] = a1.z; f.a[7] = a1.w;
         }
         float4 b0 = *reinterpret_cast<const float4 *>(Bs_k + tx * 4);
         float4 b1 = *reinterpret_cast<const float4 *>(Bs_k + 64 + tx * 4);
-        b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
-        b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+        f.b[0] = b0.x; f.b[1] = b0.y; f.b[2] = b0.z; f.b[3] = b0.w;
+        f.b[4] = b1.x; f.b[5] = b1.y; f.b[6] = b1.z; f.b[7] = b1.w;
     }
 
-    // one k step (generic operator pairs, or the FFMA2 path)
-    __device__ __forceinline__ void step1(const float (&a)[TM], const float (&b)[8], float beta) {
+    // one k step
+    __device__ __forceinline__ void step1(const Frag<TM> &f, float beta) {
 #pragma unroll
         for (int i = 0; i < TM; i++) {
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-                const float2 bb = make_float2(b[2 * j], b[2 * j + 1]);
-                if (OPC == LSB_OP_MUL && OPR == LSB_OP_ADD && !BETA) {
-                    acc[i][j] = __ffma2_rn(make_float2(a[i], a[i]), bb, acc[i][j]);
-                } else if (OPC == LSB_OP_ADD && (OPR == LSB_OP_MAX || OPR == LSB_OP_MIN) && !BETA) {
-                    float2 s = __fadd2_rn(make_float2(a[i], a[i]), bb);
+                const float2 bb = make_float2(f.b[2 * j], f.b[2 * j + 1]);
+                if constexpr (kFFMA2) {
+                    acc[i][j] = __ffma2_rn(make_float2(f.a[i], f.a[i]), bb, acc[i][j]);
+                } else if constexpr (kMAX3) {
+                    float2 s = __fadd2_rn(make_float2(f.a[i], f.a[i]), bb);
                     acc[i][j].x = Op<OPR>::apply(acc[i][j].x, s.x);
                     acc[i][j].y = Op<OPR>::apply(acc[i][j].y, s.y);
                 } else {
-                    float s0 = Op<OPC>::apply(a[i], bb.x);
-                    float s1 = Op<OPC>::apply(a[i], bb.y);
-                    if (BETA) { s0 = __fmul_rn(beta, s0); s1 = __fmul_rn(beta, s1); }
+                    float s0 = Op<OPC>::apply(f.a[i], bb.x);
+                    float s1 = Op<OPC>::apply(f.a[i], bb.y);
+                    if constexpr (BETA) { s0 = __fmul_rn(beta, s0); s1 = __fmul_rn(beta, s1); }
                     acc[i][j].x = Op<OPR>::apply(acc[i][j].x, s0);
                     acc[i][j].y = Op<OPR>::apply(acc[i][j].y, s1);
                 }
@@ -354,50 +338,87 @@ struct Micro {
         }
     }
 
-    // two k steps: the (add, max|min) path folds both into one 3-input max
-    __device__ __forceinline__ void step2(const float (&a0)[TM], const float (&b0)[8],
-                                          const float (&a1)[TM], const float (&b1)[8], float beta) {
-        if (OPC == LSB_OP_ADD && (OPR == LSB_OP_MAX || OPR == LSB_OP_MIN) && !BETA) {
+    // two k steps folded into one 3-input max/min (FADD2 + FMNMX3)
+    __device__ __forceinline__ void step2(const Frag<TM> &f0, const Frag<TM> &f1) {
 #pragma unroll
-            for (int i = 0; i < TM; i++) {
+        for (int i = 0; i < TM; i++) {
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    float2 s = __fadd2_rn(make_float2(a0[i], a0[i]), make_float2(b0[2 * j], b0[2 * j + 1]));
-                    float2 u = __fadd2_rn(make_float2(a1[i], a1[i]), make_float2(b1[2 * j], b1[2 * j + 1]));
-                    acc[i][j].x = Op<OPR>::apply(acc[i][j].x, Op<OPR>::apply(s.x, u.x));
-                    acc[i][j].y = Op<OPR>::apply(acc[i][j].y, Op<OPR>::apply(s.y, u.y));
-                }
+            for (int j = 0; j < 4; j++) {
+                float2 s = __fadd2_rn(make_float2(f0.a[i], f0.a[i]), make_float2(f0.b[2 * j], f0.b[2 * j + 1]));
+                float2 u = __fadd2_rn(make_float2(f1.a[i], f1.a[i]), make_float2(f1.b[2 * j], f1.b[2 * j + 1]));
+                acc[i][j].x = Op<OPR>::apply(acc[i][j].x, Op<OPR>::apply(s.x, u.x));
+                acc[i][j].y = Op<OPR>::apply(acc[i][j].y, Op<OPR>::apply(s.y, u.y));
+            }
+        }
+    }
+
+    // a full BK slice.  Single-step operator pairs keep the next k's fragment
+    // in flight while the current one computes; the fragment for k = 0 of the
+    // next slice is loaded by the caller-provided hook after the slice barrier.
+    template <int BM, class Boundary>
+    __device__ __forceinline__ void full_slice(float (*As)[BM + 4], float (*Bs)[kBN], int ty, int tx,
+                                               float beta, Frag<TM> (&f)[2], Boundary &&boundary) {
+        if constexpr (kMAX3) {
+#pragma unroll
+            for (int kk = 0; kk < kBK; kk += 2) {
+                Frag<TM> f1;
+                if (kk > 0) frag(As[kk], Bs[kk], ty, tx, f[0]);
+                frag(As[kk + 1], Bs[kk + 1], ty, tx, f1);
+                step2(f[0], f1);
+                // after the last pair: barrier + next slice's k = 0 into f[0]
+                // (three live fragments would not fit 128 registers)
+                if (kk == kBK - 2) boundary(f[0]);
             }
         } else {
-            step1(a0, b0, beta);
-            step1(a1, b1, beta);
+#pragma unroll
+            for (int kk = 0; kk < kBK; kk++) {
+                if (kk < kBK - 1) frag(As[kk + 1], Bs[kk + 1], ty, tx, f[(kk + 1) & 1]);
+                else boundary(f[(kk + 1) & 1]);
+                step1(f[kk & 1], beta);
+            }
         }
     }
 
     template <int BM>
-    __device__ __forceinline__ void slice(float (*As)[BM + 4], float (*Bs)[kBN], int kcount,
-                                          int ty, int tx, float beta) {
-        if (kcount == kBK) {
-#pragma unroll
-            for (int kk = 0; kk < kBK; kk += 2) {
-                float a0[TM], b0[8], a1[TM], b1[8];
-                frag(As[kk], Bs[kk], ty, tx, a0, b0);
-                frag(As[kk + 1], Bs[kk + 1], ty, tx, a1, b1);
-                step2(a0, b0, a1, b1, beta);
-            }
-        } else {
+    __device__ __forceinline__ void tail_slice(float (*As)[BM + 4], float (*Bs)[kBN], int kcount,
+                                               int ty, int tx, float beta) {
 #pragma unroll 1
-            for (int kk = 0; kk < kcount; kk++) {
-                float a0[TM], b0[8];
-                frag(As[kk], Bs[kk], ty, tx, a0, b0);
-                step1(a0, b0, beta);
-            }
+        for (int kk = 0; kk < kcount; kk++) {
+            Frag<TM> f0;
+            frag(As[kk], Bs[kk], ty, tx, f0);
+            step1(f0, beta);
         }
     }
 
     __device__ __forceinline__ float get(int i, int j) const {
-        if constexpr (TWO) return (j & 1) ? tot[i][j >> 1].y : tot[i][j >> 1].x;
         return (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
+    }
+
+    // two-level accumulation: add the chunk into the CTA-private smem total
+    // (each thread owns its slots, no barrier) and restart the chunk.
+    __device__ __forceinline__ void fold(float2 *tot) {
+        const float id = Op<OPR>::identity();
+#pragma unroll
+        for (int i = 0; i < TM; i++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                float2 *t = tot + (i * 4 + j) * kThreads + threadIdx.x;
+                float2 v = *t;
+                v.x = Op<OPR>::apply(v.x, acc[i][j].x);
+                v.y = Op<OPR>::apply(v.y, acc[i][j].y);
+                *t = v;
+                acc[i][j] = make_float2(id, id);
+            }
+    }
+    __device__ __forceinline__ void unfold(const float2 *tot) {
+#pragma unroll
+        for (int i = 0; i < TM; i++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const float2 v = tot[(i * 4 + j) * kThreads + threadIdx.x];
+                acc[i][j].x = Op<OPR>::apply(v.x, acc[i][j].x);
+                acc[i][j].y = Op<OPR>::apply(v.y, acc[i][j].y);
+            }
     }
 };
 
@@ -406,16 +427,22 @@ template <int TM>
 __device__ __forceinline__ int row_of(int ty, int i) { return (i < 4 ? 0 : 64) + ty * 4 + (i & 3); }
 __device__ __forceinline__ int col_of(int tx, int j) { return (j < 4 ? 0 : 64) + tx * 4 + (j & 3); }
 
+// dynamic shared memory of the GEMM kernel: the two-level chunk totals /
+// epilogue staging area, TM*8 floats per thread
+template <int BM>
+constexpr size_t gemm_dyn_smem() { return (size_t)(BM / 16) * 8 * kThreads * sizeof(float); }
+
 // ---------------------------------------------------------------------------
 // GEMM kernel
 // grid: x = n tiles, y = m tiles * splits, z = batch
 // ---------------------------------------------------------------------------
 
 template <int OPC, int OPR, bool BETA, int BM, bool TWO = false>
-__global__ void __launch_bounds__(kThreads, BM == 128 ? LSB_MINB128 : 2) semiring_gemm_kernel(const GemmArgs p) {
+__global__ void __launch_bounds__(kThreads, 2) semiring_gemm_kernel(const GemmArgs p) {
     constexpr int TM = BM / 16;
     __shared__ __align__(16) float As[2][kBK][BM + 4];
     __shared__ __align__(16) float Bs[2][kBK][kBN];
+    extern __shared__ __align__(16) float2 stage2[];   // [TM*4][kThreads] float2
 
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int64_t m_tiles = (p.M + BM - 1) / BM;
@@ -426,33 +453,48 @@ __global__ void __launch_bounds__(kThreads, BM == 128 ? LSB_MINB128 : 2) semirin
     const int64_t kbeg = split * p.k_per_split;
     const int64_t kend = min(p.K, kbeg + p.k_per_split);
 
-    Micro<OPC, OPR, BETA, TM, TWO> mk;
+    using MK = Micro<OPC, OPR, BETA, TM>;
+    MK mk;
     mk.init();
+    if constexpr (TWO) {
+        const float id = Op<OPR>::identity();
+        for (int e = threadIdx.x; e < TM * 4 * kThreads; e += kThreads) stage2[e] = make_float2(id, id);
+    }
     GemmLoader<BM> ld;
 
     if (kbeg < kend) {
         ld.load(p, bz, m0, n0, kbeg, kend);
         ld.store(p, As[0], Bs[0]);
         __syncthreads();
+        Frag<TM> f[2];
+        MK::frag(As[0][0], Bs[0][0], ty, tx, f[0]);
         int buf = 0;
         int chunk = 0;
         for (int64_t k0 = kbeg; k0 < kend; k0 += kBK) {
             const bool more = k0 + kBK < kend;
             if (more) ld.load(p, bz, m0, n0, k0 + kBK, kend);
-            const int kcount = (int)min((int64_t)kBK, kend - k0);
-            mk.template slice<BM>(As[buf], Bs[buf], kcount, ty, tx, p.beta);
+            if (k0 + kBK <= kend) {
+                // barrier + next slice's first fragment, issued before the
+                // last k step of this slice so its latency overlaps the math
+                auto boundary = [&](Frag<TM> &nf) {
+                    if (more) ld.store(p, As[buf ^ 1], Bs[buf ^ 1]);
+                    __syncthreads();
+                    if (more) MK::frag(As[buf ^ 1][0], Bs[buf ^ 1][0], ty, tx, nf);
+                };
+                mk.template full_slice<BM>(As[buf], Bs[buf], ty, tx, p.beta, f, boundary);
+            } else {
+                mk.template tail_slice<BM>(As[buf], Bs[buf], (int)(kend - k0), ty, tx, p.beta);
+            }
             if constexpr (TWO) {
                 if (++chunk == kChunkSlices) {
-                    mk.fold();
+                    mk.fold(stage2);
                     chunk = 0;
                 }
             }
-            if (more) ld.store(p, As[buf ^ 1], Bs[buf ^ 1]);
-            __syncthreads();
             buf ^= 1;
         }
     }
-    mk.fold();
+    if constexpr (TWO) mk.unfold(stage2);
 
     // ---- epilogue
     if (p.ws != nullptr) {
@@ -471,27 +513,50 @@ __global__ void __launch_bounds__(kThreads, BM == 128 ? LSB_MINB128 : 2) semirin
         return;
     }
     float *C = p.C + bz * p.sc_b;
+    if (p.epi.n == 0) {
 #pragma unroll
-    for (int i = 0; i < TM; i++) {
-        int64_t m = m0 + row_of<TM>(ty, i);
+        for (int i = 0; i < TM; i++) {
+            int64_t m = m0 + row_of<TM>(ty, i);
+            if (m >= p.M) continue;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                int64_t nq = n0 + h * 64 + tx * 4;
+                if (p.c_vec && nq + 3 < p.N) {
+                    *reinterpret_cast<float4 *>(C + m * p.sc_m + nq) =
+                        make_float4(mk.get(i, h * 4), mk.get(i, h * 4 + 1), mk.get(i, h * 4 + 2), mk.get(i, h * 4 + 3));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (nq + q < p.N) C[m * p.sc_m + (nq + q) * p.sc_n] = mk.get(i, h * 4 + q);
+                }
+            }
+        }
+        return;
+    }
+    // fused epilogue: stage the accumulators through shared memory so the
+    // epilogue code is instantiated once (a rolled loop), not TM*8 times
+    float *stage = reinterpret_cast<float *>(stage2);
+#pragma unroll
+    for (int i = 0; i < TM; i++)
+#pragma unroll
+        for (int j = 0; j < 8; j++) stage[(i * 8 + j) * kThreads + threadIdx.x] = mk.get(i, j);
+#pragma unroll 1
+    for (int e = 0; e < TM * 2; e++) {
+        const int i = e >> 1, h = e & 1;
+        const int64_t m = m0 + row_of<TM>(ty, i);
         if (m >= p.M) continue;
+        const int64_t nq = n0 + h * 64 + tx * 4;
+        float v[4];
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            int64_t nq = n0 + h * 64 + tx * 4;
-            float v[4];
+        for (int q = 0; q < 4; q++)
+            v[q] = apply_epilogue(p.epi, stage[(i * 8 + h * 4 + q) * kThreads + threadIdx.x], bz, m,
+                                  nq + q, 0);
+        if (p.c_vec && nq + 3 < p.N) {
+            *reinterpret_cast<float4 *>(C + m * p.sc_m + nq) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                float x = mk.get(i, h * 4 + q);
-                if (p.epi.n) x = apply_epilogue(p.epi, x, bz, m, nq + q, 0);
-                v[q] = x;
-            }
-            if (p.c_vec && nq + 3 < p.N) {
-                *reinterpret_cast<float4 *>(C + m * p.sc_m + nq) = make_float4(v[0], v[1], v[2], v[3]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 4; q++)
-                    if (nq + q < p.N) C[m * p.sc_m + (nq + q) * p.sc_n] = v[q];
-            }
+            for (int q = 0; q < 4; q++)
+                if (nq + q < p.N) C[m * p.sc_m + (nq + q) * p.sc_n] = v[q];
         }
     }
 }
@@ -540,19 +605,28 @@ __global__ void __launch_bounds__(kThreads, 2) conv_igemm_kernel(const ConvArgs 
     ld.init(p, img, n0);
     __syncthreads();
 
-    Micro<OPC, OPR, BETA, TM> mk;
+    using MK = Micro<OPC, OPR, BETA, TM>;
+    MK mk;
     mk.init();
     ld.load<BM>(p, koff, krs, m0, 0, p.K);
     ld.store<BM>(p, As[0], Bs[0]);
     __syncthreads();
+    Frag<TM> f[2];
+    MK::frag(As[0][0], Bs[0][0], ty, tx, f[0]);
     int buf = 0;
     for (int64_t k0 = 0; k0 < p.K; k0 += kBK) {
         const bool more = k0 + kBK < p.K;
         if (more) ld.load<BM>(p, koff, krs, m0, k0 + kBK, p.K);
-        const int kcount = (int)min((int64_t)kBK, p.K - k0);
-        mk.template slice<BM>(As[buf], Bs[buf], kcount, ty, tx, p.beta);
-        if (more) ld.store<BM>(p, As[buf ^ 1], Bs[buf ^ 1]);
-        __syncthreads();
+        if (k0 + kBK <= p.K) {
+            auto boundary = [&](Frag<TM> &nf) {
+                if (more) ld.store<BM>(p, As[buf ^ 1], Bs[buf ^ 1]);
+                __syncthreads();
+                if (more) MK::frag(As[buf ^ 1][0], Bs[buf ^ 1][0], ty, tx, nf);
+            };
+            mk.template full_slice<BM>(As[buf], Bs[buf], ty, tx, p.beta, f, boundary);
+        } else {
+            mk.template tail_slice<BM>(As[buf], Bs[buf], (int)(p.K - k0), ty, tx, p.beta);
+        }
         buf ^= 1;
     }
 
