@@ -182,6 +182,10 @@ int lsb_stream_sync(void *stream);
 
 /* ---- kernels ---------------------------------------------------------------- */
 int lsb_semiring_gemm(const lsb_gemm_desc *desc, void *stream);
+/* the LSB_ALGO_* lsb_semiring_gemm will use for `desc` (AUTO resolved:
+ * 3xTF32 tensor cores for large batch-1 (mul, add) contractions, else the
+ * SIMT semiring kernel); < 0 if an explicit request cannot be honoured */
+int lsb_gemm_algo(const lsb_gemm_desc *desc);
 int lsb_conv2d_nchw(const lsb_conv_desc *desc, void *stream);
 int lsb_affine_nest(const lsb_nest_desc *desc, void *stream);
 

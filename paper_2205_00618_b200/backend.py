@@ -67,7 +67,11 @@ class LaunchProgram:
     var_names: list = field(default_factory=list)
 
     def disassemble(self) -> str:
-        return "".join(f"{r.op} {r.step.describe()}\n" for r in self.instrs)
+        out = []
+        for r in self.instrs:
+            algo = r.step.params.get("algo_selected")
+            out.append(f"{r.op} {r.step.describe()}" + (f" algo={algo}" if algo else "") + "\n")
+        return "".join(out)
 
     def encode(self):
         raise NotImplementedError("B200 launch programs are not VM-encodable")
@@ -232,6 +236,7 @@ class Runner:
                 d.split_k = p.get("split_k", 0)
                 d.tile_m = p.get("tile_hint", 0)
                 d.m_begin, d.m_end = p.get("m_begin", 0), p.get("m_end", 0)
+                p["algo_selected"] = native.gemm_algo(d)
                 descs.append((native.semiring_gemm, d))
             elif step.kind == "conv":
                 d = native.ConvDesc()

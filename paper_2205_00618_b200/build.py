@@ -28,7 +28,7 @@ LIB = os.path.join(PKG, "liblsb.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-Xptxas", "-warn-spills"]
-UNITS = ["lsb_api.cu", "kern_fast.cu", "kern_generic.cu", "kern_nest.cu"]
+UNITS = ["lsb_api.cu", "kern_fast.cu", "kern_generic.cu", "kern_nest.cu", "kern_tf32.cu"]
 
 
 def nvcc() -> str:

@@ -1,0 +1,111 @@
+// kern_tf32.cu -- host side of the 3xTF32 tcgen05 path: split prepass,
+// TMA tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry
+// point, so liblsb.so needs no -lcuda), launch.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "lsb_dispatch.cuh"
+#include "tf32x3_gemm.cuh"
+
+namespace lsb {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::mutex g_tc_mu;
+float *g_split = nullptr;
+size_t g_split_bytes = 0;
+
+bool load_encode() {
+    if (g_encode) return true;
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fn == nullptr)
+        return false;
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    return true;
+}
+
+bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp) {
+    cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)kp * sizeof(float)};
+    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)tc::BM};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool tf32x3_supported(int64_t M, int64_t N, int64_t K) {
+    return M >= 1 && N >= 1 && K >= 1 && M <= (1ll << 31) && N <= (1ll << 31) && load_encode();
+}
+
+// returns 0 on success, else a negative LSB_ERR_* with `err` filled
+int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, int64_t sa_k, const float *B,
+                int64_t sb_k, int64_t sb_n, float *C, int64_t sc_m, int64_t sc_n, int c_vec, const EpiStages &epi,
+                cudaStream_t s, char *err, size_t errlen) {
+    if (!load_encode()) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
+        return LSB_ERR_UNSUPPORTED;
+    }
+    const int64_t Kp = (K + tc::BK - 1) / tc::BK * tc::BK;
+    const size_t need = sizeof(float) * (size_t)(2 * M + 2 * N) * (size_t)Kp;
+    float *ws;
+    {
+        std::lock_guard<std::mutex> lk(g_tc_mu);
+        if (need > g_split_bytes) {
+            if (g_split) {
+                cudaDeviceSynchronize();
+                cudaFree(g_split);
+                g_split = nullptr;
+                g_split_bytes = 0;
+            }
+            if (cudaMalloc(&g_split, need) != cudaSuccess) {
+                snprintf(err, errlen, "cudaMalloc(%zu) for the tf32 split operands failed", need);
+                return LSB_ERR_NOMEM;
+            }
+            g_split_bytes = need;
+        }
+        ws = g_split;
+    }
+    float *ahi = ws, *alo = ahi + M * Kp, *bhi = alo + M * Kp, *blo = bhi + N * Kp;
+    {
+        dim3 ga((unsigned)((Kp + 31) / 32), (unsigned)((M + 31) / 32));
+        tc::tf32_split_kernel<<<ga, 256, 0, s>>>(A, M, K, sa_m, sa_k, ahi, alo, Kp);
+        dim3 gb((unsigned)((Kp + 31) / 32), (unsigned)((N + 31) / 32));
+        tc::tf32_split_kernel<<<gb, 256, 0, s>>>(B, N, K, sb_n, sb_k, bhi, blo, Kp);
+    }
+    CUtensorMap mah, mal, mbh, mbl;
+    if (!make_map(&mah, ahi, M, Kp) || !make_map(&mal, alo, M, Kp) || !make_map(&mbh, bhi, N, Kp) ||
+        !make_map(&mbl, blo, N, Kp)) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
+        return LSB_ERR_CUDA;
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tc::tf32x3_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc::kSmemBytes);
+        attr = true;
+    }
+    tc::TcArgs a;
+    memset(&a, 0, sizeof(a));
+    a.M = M; a.N = N; a.K = K; a.Kp = Kp;
+    a.C = C; a.sc_m = sc_m; a.sc_n = sc_n; a.c_vec = c_vec;
+    a.epi = epi;
+    a.m_tiles = (int)((M + tc::BM - 1) / tc::BM);
+    a.n_tiles = (int)((N + tc::BN - 1) / tc::BN);
+    dim3 grid((unsigned)(a.m_tiles * a.n_tiles));
+    tc::tf32x3_gemm_kernel<<<grid, tc::kThreadsTC, tc::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
+    return LSB_OK;
+}
+
+}  // namespace lsb

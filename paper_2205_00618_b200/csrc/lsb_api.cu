@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -139,9 +140,33 @@ int pick_mode_b(const lsb_gemm_desc *d) {
     return lsb::LD_GENERIC;
 }
 
+// GEMM algorithm the launcher uses for this descriptor (M = rows actually
+// computed); -1 when an explicit request cannot be honoured
+int select_algo(const lsb_gemm_desc *d, int64_t M) {
+    int algo = d->algo;
+    if (const char *env = getenv("LSB_GEMM_ALGO")) {
+        if (!strcmp(env, "simt")) algo = LSB_ALGO_SIMT;
+        else if (!strcmp(env, "tf32x3")) algo = LSB_ALGO_TF32X3;
+    }
+    const bool tc_ok = d->combine == LSB_OP_MUL && d->reduce == LSB_OP_ADD && !d->beta_in_loop &&
+                       d->batch == 1 && d->K > 0;
+    if (algo == LSB_ALGO_TF32X3) return tc_ok ? algo : -1;
+    if (algo == LSB_ALGO_AUTO && tc_ok && M >= 128 && d->N >= 128 && d->K >= 256 &&
+        (double)M * d->N * d->K >= (double)(1ll << 30) && lsb::tf32x3_supported(M, d->N, d->K))
+        return LSB_ALGO_TF32X3;
+    return LSB_ALGO_SIMT;
+}
+
 }  // namespace
 
 extern "C" {
+
+int lsb_gemm_algo(const lsb_gemm_desc *d) {
+    if (!d) return fail(LSB_ERR_INVALID, "null desc");
+    const int64_t m_begin = std::max<int64_t>(0, d->m_begin);
+    const int64_t m_end = d->m_end > 0 ? std::min(d->m_end, d->M) : d->M;
+    return select_algo(d, m_end - m_begin);
+}
 
 int lsb_abi_version(void) { return LSB_ABI_VERSION; }
 
@@ -236,7 +261,6 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     if (!d->A || !d->B || !d->C) return fail(LSB_ERR_INVALID, "null operand");
     int rc = check_epi(d->n_epi, d->epi);
     if (rc) return rc;
-    if (d->algo == LSB_ALGO_TF32X3) return fail(LSB_ERR_UNSUPPORTED, "tf32x3 path not built");
     cudaStream_t s = (cudaStream_t)stream;
 
     int64_t m_begin = std::max<int64_t>(0, d->m_begin);
@@ -262,6 +286,20 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     a.a_mode = pick_mode_a(&dd, d->sa_m, d->sa_k);
     a.b_mode = pick_mode_b(&dd);
     a.c_vec = (d->sc_n == 1 && aligned16(a.C) && d->sc_m % 4 == 0 && (d->batch == 1 || d->sc_b % 4 == 0)) ? 1 : 0;
+
+    // ---- algorithm: 3xTF32 tensor cores for large fp32 (mul, add) contractions
+    const int algo = select_algo(d, M);
+    if (algo < 0) return fail(LSB_ERR_UNSUPPORTED, "tf32x3 covers batch-1 (mul, add) contractions");
+    if (algo == LSB_ALGO_TF32X3) {
+        char err[256] = "";
+        rc = lsb::tf32x3_gemm(M, d->N, d->K, a.A, d->sa_m, d->sa_k, d->B, d->sb_k, d->sb_n, a.C, d->sc_m,
+                              d->sc_n, a.c_vec, a.epi, s, err, sizeof(err));
+        if (rc) return fail(rc, "%s", err);
+        rc = check_launch("tf32x3_gemm");
+        if (rc) return rc;
+        g_launches.fetch_add(2, std::memory_order_relaxed);   // + the two split prepasses
+        return LSB_OK;
+    }
 
     if (d->K == 0) {
         // empty reduction: every output is the reduce identity, then the epilogue

@@ -1,0 +1,369 @@
+// tf32x3_gemm.cuh -- fp32-accurate (mul, add) contraction on the 5th-gen
+// tensor cores: split-TF32 ("3xTF32") with tcgen05.mma, TMEM accumulators,
+// TMA + mbarrier pipelines, warp-specialised roles.
+//
+//   C = A.B  ~=  Ahi.Bhi + Ahi.Blo + Alo.Bhi        hi = rna_tf32(x), lo = rna_tf32(x - hi)
+//
+// The dropped Alo.Blo term is ~2^-22 relative; each split keeps ~2^-23, so a
+// product carries ~fp32 error.  Accumulation is two-level: the tensor core
+// accumulates one K chunk (kChunkK) into a TMEM buffer, the epilogue warps
+// fold finished chunks into fp32 registers (round-to-nearest) while the MMA
+// warp fills the other TMEM buffer.  The chunk is short because the tensor
+// core's fp32 accumulate truncates: measured on B200, 256-K chunks fail the
+// strict 1e-5 + 1e-4|ref| rule on ~0.1% of elements at K = 1024; a numpy model
+// of truncating accumulation reproduces that and passes at 64-K chunks.
+//
+// Prepass (tf32_split_kernel): A -> Ahi/Alo [M][Kp], B -> Bhi/Blo [N][Kp],
+// both K-major (B transposed) so every UMMA operand is the canonical K-major
+// SWIZZLE_128B layout; any input strides are handled here.
+//
+// Main kernel, one CTA per 128x128 output tile, 192 threads:
+//   warp 0      TMA producer: 4 tiles (Ahi, Alo, Bhi, Blo) per K=32 stage
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5   epilogue: TMEM -> registers (chunk fold) -> smem -> fused
+//               elementwise epilogue -> coalesced global stores
+#pragma once
+
+#include <cuda.h>
+
+#include "lsb_common.cuh"
+
+namespace lsb {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int BK = 32;                 // 32 fp32 = 128 B = one SWIZZLE_128B row
+constexpr int STAGES = 3;
+constexpr int kChunkK = 64;            // K per TMEM accumulation chunk (see below)
+constexpr int kChunkStages = kChunkK / BK;
+constexpr int kThreadsTC = 192;
+constexpr int kTileBytes = BM * BK * 4;              // 16 KiB (A or B, hi or lo)
+constexpr int kStageBytes = 4 * kTileBytes;          // 64 KiB
+constexpr int kTmemCols = 2 * BN;                    // two chunk accumulators
+constexpr size_t kSmemBytes = (size_t)STAGES * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+constexpr int kGroupM = 16;            // tile raster: 16 m-tiles per group share B in L2
+
+struct TcArgs {
+    int64_t M, N, K, Kp;
+    int m_tiles, n_tiles;
+    float *C; int64_t sc_m, sc_n;
+    int c_vec;
+    EpiStages epi;
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    while (!mbar_try_wait(bar, phase)) {
+    }
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *bar, void *dst, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major operand tile in the canonical SWIZZLE_128B layout: rows of 128 B,
+// 8-row (1024 B) swizzle atoms stacked with SBO = 1024 B.
+__device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);   // start address (16 B units)
+    d |= (uint64_t)1 << 16;                    // leading byte offset (unused when swizzled)
+    d |= (uint64_t)(1024 >> 4) << 32;          // stride byte offset
+    d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                    // layout: SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor: kind::tf32, fp32 accumulate, A/B K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+// 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// ---------------------------------------------------------------- prepass
+
+// X element (r, k) = X[r*s_r + k*s_k]  ->  hi/lo[r][k] (row-major, Kp columns,
+// zero padded).  32x32 tiles through smem so both the read (whichever stride
+// is 1) and the write (k fastest) are coalesced.
+__global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict__ X, int64_t R, int64_t Kd,
+                                                         int64_t s_r, int64_t s_k, float *__restrict__ hi,
+                                                         float *__restrict__ lo, int64_t Kp) {
+    __shared__ float tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+    const bool r_fast = (s_r == 1 && s_k != 1);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        int a = ty + 8 * j;   // slow index within the tile
+        int64_t r = r_fast ? r0 + tx : r0 + a;
+        int64_t k = r_fast ? k0 + a : k0 + tx;
+        float v = (r < R && k < Kd) ? __ldg(X + r * s_r + k * s_k) : 0.0f;
+        if (r_fast) tile[tx][a] = v; else tile[a][tx] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        int a = ty + 8 * j;
+        int64_t r = r0 + a, k = k0 + tx;
+        if (r < R && k < Kp) {
+            float x = tile[a][tx];
+            float h = rna_tf32(x);
+            hi[r * Kp + k] = h;
+            lo[r * Kp + k] = rna_tf32(x - h);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- main kernel
+
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    tf32x3_gemm_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                       const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                       const TcArgs p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the SWIZZLE_128B atoms
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * kStageBytes);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;    // [2] chunk accumulator ready
+    uint64_t *tempty = tfull + 2;        // [2] chunk accumulator drained
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // grouped raster: consecutive CTAs walk kGroupM m-tiles before moving to
+    // the next n-tile, so the CTAs resident together share A and B blocks
+    int mt, nt;
+    {
+        const int t = blockIdx.x;
+        const int per_group = kGroupM * p.n_tiles;
+        const int g = t / per_group, first_m = g * kGroupM;
+        const int gm = min(kGroupM, p.m_tiles - first_m);
+        const int r = t % per_group;
+        mt = first_m + r % gm;
+        nt = r / gm;
+    }
+    const int64_t m0 = (int64_t)mt * BM, n0 = (int64_t)nt * BN;
+    const int num_kb = (int)(p.Kp / BK);
+    const int num_chunks = (num_kb + kChunkStages - 1) / kChunkStages;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&map_ahi);
+        tma_prefetch_desc(&map_alo);
+        tma_prefetch_desc(&map_bhi);
+        tma_prefetch_desc(&map_blo);
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);   // one arrive per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int kb = 0; kb < num_kb; kb++) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                unsigned char *base = smem + stage * kStageBytes;
+                mbar_expect_tx(&full[stage], kStageBytes);
+                const int kx = kb * BK;
+                tma_load_2d(&map_ahi, &full[stage], base, kx, (int)m0);
+                tma_load_2d(&map_alo, &full[stage], base + kTileBytes, kx, (int)m0);
+                tma_load_2d(&map_bhi, &full[stage], base + 2 * kTileBytes, kx, (int)n0);
+                tma_load_2d(&map_blo, &full[stage], base + 3 * kTileBytes, kx, (int)n0);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (one thread)
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int c = 0; c < num_chunks; c++) {
+                const int b = c & 1;
+                const uint32_t tphase = (uint32_t)((c >> 1) & 1);
+                mbar_wait(&tempty[b], tphase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(b * BN);
+                const int kb_end = min(num_kb, (c + 1) * kChunkStages);
+                for (int kb = c * kChunkStages; kb < kb_end; kb++) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t base = smem_u32(smem + stage * kStageBytes);
+                    const uint64_t ahi = sdesc_k_sw128(base), alo = sdesc_k_sw128(base + kTileBytes);
+                    const uint64_t bhi = sdesc_k_sw128(base + 2 * kTileBytes),
+                                   blo = sdesc_k_sw128(base + 3 * kTileBytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 8; k++) {
+                        const uint64_t off = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along K
+                        const uint32_t first = (kb == c * kChunkStages && k == 0) ? 0u : 1u;
+                        umma_tf32(d, ahi + off, bhi + off, idesc, first);
+                        umma_tf32(d, ahi + off, blo + off, idesc, 1u);
+                        umma_tf32(d, alo + off, bhi + off, idesc, 1u);
+                    }
+                    umma_commit(&empty[stage]);   // smem slot free once these MMAs retire
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[b]);           // chunk accumulator complete
+            }
+        }
+    } else {
+        // ---------------- epilogue warps 2..5
+        const int q = warp & 3;                   // TMEM lane quadrant of this warp
+        const int row = q * 32 + lane;
+        float tot[BN];
+#pragma unroll
+        for (int i = 0; i < BN; i++) tot[i] = 0.0f;
+        for (int c = 0; c < num_chunks; c++) {
+            const int b = c & 1;
+            mbar_wait(&tfull[b], (uint32_t)((c >> 1) & 1));
+            tc_fence_after();
+#pragma unroll
+            for (int part = 0; part < BN / 32; part++) {
+                float v[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + part * 32), v);
+#pragma unroll
+                for (int i = 0; i < 32; i++) tot[part * 32 + i] += v[i];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[b]);
+        }
+        // stage the tile in (now idle) pipeline smem: row-major, 16-B chunks
+        // XOR-swizzled by row so both the write and the read are conflict-free
+        float *tile = reinterpret_cast<float *>(smem);
+        // every TMA load was consumed by an MMA whose completion preceded the
+        // last tfull arrive, so the stage buffers are free
+#pragma unroll
+        for (int ch = 0; ch < BN / 4; ch++) {
+            const int pos = ch ^ (row & 31);
+            *reinterpret_cast<float4 *>(tile + row * BN + pos * 4) =
+                make_float4(tot[ch * 4], tot[ch * 4 + 1], tot[ch * 4 + 2], tot[ch * 4 + 3]);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // epilogue warps only
+        const int ew = warp - 2;                          // 0..3, 32 rows each
+#pragma unroll 1
+        for (int rr = 0; rr < 32; rr++) {
+            const int r = ew * 32 + rr;
+            const int64_t m = m0 + r;
+            if (m >= p.M) continue;
+            const int pos = lane ^ (r & 31);
+            float4 v = *reinterpret_cast<const float4 *>(tile + r * BN + pos * 4);
+            const int64_t n = n0 + lane * 4;
+            float x[4] = {v.x, v.y, v.z, v.w};
+            if (p.epi.n) {
+#pragma unroll
+                for (int e = 0; e < 4; e++) x[e] = apply_epilogue(p.epi, x[e], 0, m, n + e, 0);
+            }
+            float *dst = p.C + m * p.sc_m;
+            if (p.c_vec && n + 3 < p.N) {
+                *reinterpret_cast<float4 *>(dst + n) = make_float4(x[0], x[1], x[2], x[3]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; e++)
+                    if (n + e < p.N) dst[(n + e) * p.sc_n] = x[e];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    }
+}
+
+}  // namespace tc
+}  // namespace lsb

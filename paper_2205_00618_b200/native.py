@@ -100,6 +100,7 @@ _SIGS = {
     "lsb_memcpy_d2d": ([vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
     "lsb_stream_sync": ([vp], ctypes.c_int),
     "lsb_semiring_gemm": ([ctypes.POINTER(GemmDesc), vp], ctypes.c_int),
+    "lsb_gemm_algo": ([ctypes.POINTER(GemmDesc)], ctypes.c_int),
     "lsb_conv2d_nchw": ([ctypes.POINTER(ConvDesc), vp], ctypes.c_int),
     "lsb_affine_nest": ([ctypes.POINTER(NestDesc), vp], ctypes.c_int),
     "lsb_launch_count": ([ctypes.c_int], ctypes.c_int64),
@@ -232,6 +233,14 @@ def sync(stream: int = 0) -> None:
 
 def semiring_gemm(desc: GemmDesc, stream: int = 0) -> None:
     check(lib().lsb_semiring_gemm(ctypes.byref(desc), vp(stream)), "lsb_semiring_gemm")
+
+
+ALGO_NAMES = {0: "auto", 1: "simt", 2: "tf32x3"}
+
+
+def gemm_algo(desc: GemmDesc) -> str:
+    """Algorithm lsb_semiring_gemm picks for ``desc`` (simt | tf32x3)."""
+    return ALGO_NAMES.get(int(lib().lsb_gemm_algo(ctypes.byref(desc))), "invalid")
 
 
 def conv2d_nchw(desc: ConvDesc, stream: int = 0) -> None:
