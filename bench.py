@@ -376,6 +376,17 @@ def run_gpu(args):
                 per_config[other] = {"desc": CONFIGS[other]["desc"], "GFLOP/s": round(g, 1),
                                      "ms": round(t, 4), "frac_fp32_peak": round(g / 1e3 / fp32_peak, 4),
                                      "kernels": r["steps"]}
+                if CONFIGS[other].get("reduce") == "max":
+                    # measured on this B200 (profiles/r01_ubench_pipes_maxplus.log):
+                    # FADD2 and FMNMX3 share issue at 0.5 warp-instr/clk/SMSP, so
+                    # one max-plus point (2 "flop") costs 1/32 of an SMSP cycle:
+                    # the max-plus ceiling is half the FP32 FFMA peak
+                    ceil = fp32_peak / 2.0
+                    per_config[other]["maxplus_issue_ceiling_tflops"] = round(ceil, 2)
+                    per_config[other]["frac_maxplus_ceiling"] = round(g / 1e3 / ceil, 4)
+                if any("tf32x3" in s for s in r["steps"]) and pk.get("bf16_tflops_sustained"):
+                    ceil = pk["bf16_tflops_sustained"] / 6.0
+                    per_config[other]["frac_tf32x3_ceiling"] = round(g / 1e3 / ceil, 4)
             except Exception as e:  # report, never hide
                 per_config[other] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0 and world == 1 and not args.no_cpu:
