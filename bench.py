@@ -264,9 +264,19 @@ def gpu_config_run(name: str, steps: int, warmup: int, torch, rank: int, world: 
     if world > 1:
         torch.distributed.barrier()
     launches = per_step * steps
+    # dominant kernel alone (the contraction launch, not its prepass / fold):
+    # CUDA events placed by liblsb around that launch on the same stream
+    kernel_ms = []
+    native.profile(True)
+    for _ in range(min(steps, 3)):
+        if flush is not None:
+            flush.zero_()
+        backend.run_device(k, ptrs, sh)
+        kernel_ms.append(native.last_kernel_ms())
+    native.profile(False)
     times = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     res = {"ms_total": sum(times), "ms_mean": sum(times) / steps, "ms_min": min(times),
-           "launches": launches,
+           "kernel_ms": sum(kernel_ms) / len(kernel_ms), "launches": launches,
            "steps": [s.kind + (f":{s.params['algo_selected']}" if s.params.get("algo_selected") else "")
                      for s in k.plan.steps],
            "kernel_launches_per_step": len(k.plan.steps)}
@@ -303,6 +313,20 @@ def gpu_config_run(name: str, steps: int, warmup: int, torch, rank: int, world: 
             pb.close()
     del tens
     return res
+
+
+def traffic_of(name: str, steps) -> float | None:
+    """dram read+write bytes per launch of the dominant kernel, from the
+    committed `ncu --set full` capture of the same kernel/shape
+    (profiles/traffic.json, written by tools/ncu_summary.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+    except Exception:
+        return None
+    algo = "tf32x3" if any("tf32x3" in s for s in steps) else "simt"
+    ent = t.get(f"{name}_{algo}")
+    return ent["dram_bytes_per_launch"] if ent else None
 
 
 def roofline(steps, achieved, fp32_peak, sm_max, info, clocks, pk) -> dict:
@@ -360,7 +384,9 @@ def run_gpu(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms, e2e_ms, _ = t.tolist()
     value = total_flops / (ms * 1e-3) / 1e9
-    achieved = flops_rank / (res["ms_mean"] * 1e-3) / 1e12
+    # roofline numerator: algorithmic flops of the dominant launch / its own
+    # average duration (CUDA events around that launch, measured live)
+    achieved = flops_rank / (res["kernel_ms"] * 1e-3) / 1e12
 
     per_config = {}
     cpu = None
@@ -407,7 +433,9 @@ def run_gpu(args):
                        "rows_per_rank": (CONFIGS[name].get("M", 0) // world) if name == "C5" else None,
                        "parallelism": f"row-shard x{world}" if world > 1 else "single",
                        "l2": "inputs 2 GiB > 126 MB L2" if name == "C5" else "L2 flushed between steps"},
-            "roofline": roofline(res["steps"], achieved, fp32_peak, sm_max, info, clocks, pk),
+            "roofline": {**roofline(res["steps"], achieved, fp32_peak, sm_max, info, clocks, pk),
+                         "traffic": traffic_of(name, res["steps"]),
+                         "kernel_ms": round(res["kernel_ms"], 4), "step_ms": round(res["ms_mean"], 4)},
             "e2e": {"value": round(total_flops / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GFLOP/s",
                     "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": int(res.get("h2d", 0)), "d2h_bytes_per_step": int(res.get("d2h", 0)),

@@ -189,6 +189,13 @@ int lsb_gemm_algo(const lsb_gemm_desc *desc);
 int lsb_conv2d_nchw(const lsb_conv_desc *desc, void *stream);
 int lsb_affine_nest(const lsb_nest_desc *desc, void *stream);
 
+/* per-kernel timing for rooflines: when enabled, the dominant kernel of each
+ * lsb_semiring_gemm call (the contraction, not its prepass / fold) is
+ * bracketed by CUDA events on the call's stream; lsb_last_kernel_ms waits for
+ * and returns the most recent one.  Not for use inside graph capture. */
+int lsb_profile(int enable);
+int lsb_last_kernel_ms(float *ms);
+
 /* sizeof of the descriptor structs (which: 0 gemm, 1 conv, 2 nest, 3 epi
  * stage) so bindings can verify their layout without a GPU */
 int64_t lsb_sizeof(int which);

@@ -104,7 +104,9 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     a.m_tiles = (int)((M + tc::BM - 1) / tc::BM);
     a.n_tiles = (int)((N + tc::BN - 1) / tc::BN);
     dim3 grid((unsigned)(a.m_tiles * a.n_tiles));
+    prof_mark(0, s);
     tc::tf32x3_gemm_kernel<<<grid, tc::kThreadsTC, tc::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
+    prof_mark(1, s);
     return LSB_OK;
 }
 

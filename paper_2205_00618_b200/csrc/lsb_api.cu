@@ -51,6 +51,15 @@ int sm_count();
 int lsb::device_sms() { return sm_count(); }
 
 namespace {
+bool g_prof = false;
+cudaEvent_t g_prof_ev[2] = {nullptr, nullptr};
+}  // namespace
+
+void lsb::prof_mark(int which, cudaStream_t s) {
+    if (g_prof && g_prof_ev[which]) cudaEventRecord(g_prof_ev[which], s);
+}
+
+namespace {
 
 int sm_count() {
     if (g_sm_count == 0) {
@@ -237,6 +246,23 @@ int lsb_stream_sync(void *stream) {
     return LSB_OK;
 }
 
+int lsb_profile(int enable) {
+    if (enable && !g_prof_ev[0]) {
+        LSB_CUDA(cudaEventCreate(&g_prof_ev[0]));
+        LSB_CUDA(cudaEventCreate(&g_prof_ev[1]));
+    }
+    g_prof = enable != 0;
+    return LSB_OK;
+}
+
+int lsb_last_kernel_ms(float *ms) {
+    if (!ms) return fail(LSB_ERR_INVALID, "null out");
+    if (!g_prof_ev[0]) return fail(LSB_ERR_INVALID, "profiling was never enabled");
+    LSB_CUDA(cudaEventSynchronize(g_prof_ev[1]));
+    LSB_CUDA(cudaEventElapsedTime(ms, g_prof_ev[0], g_prof_ev[1]));
+    return LSB_OK;
+}
+
 int64_t lsb_sizeof(int which) {
     switch (which) {
     case 0: return (int64_t)sizeof(lsb_gemm_desc);
@@ -355,7 +381,9 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
         if (rc) return rc;
     }
     dim3 grid((unsigned)n_tiles, (unsigned)(m_tiles * splits), (unsigned)d->batch);
+    lsb::prof_mark(0, s);
     fn(a, grid, s);
+    lsb::prof_mark(1, s);
     rc = check_launch("semiring_gemm");
     if (rc) return rc;
     if (splits > 1) {
@@ -397,7 +425,9 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     const int bm = 64;
     dim3 grid((unsigned)((a.N + lsb::kBN - 1) / lsb::kBN), (unsigned)((a.M + bm - 1) / bm), (unsigned)d->N);
     size_t dyn = (size_t)K * (sizeof(int64_t) + sizeof(int2));
+    lsb::prof_mark(0, (cudaStream_t)stream);
     lsb::launch_conv_fast(a, grid, dyn, (cudaStream_t)stream);
+    lsb::prof_mark(1, (cudaStream_t)stream);
     return check_launch("conv_igemm");
 }
 

@@ -13,6 +13,9 @@ using SplitFn = void (*)(const GemmArgs &, int64_t, cudaStream_t);
 using NestFn = void (*)(const NestArgs &, cudaStream_t);
 
 int device_sms();                               // lsb_api.cu
+// optional timing of the dominant kernel of a call (lsb_profile): which = 0
+// before its launch, 1 after; no-op unless profiling is enabled
+void prof_mark(int which, cudaStream_t s);
 
 GemmFn fast_gemm(int combine, int reduce, int bm, bool two_level);   // kern_fast.cu (nullptr if untuned)
 void launch_conv_fast(const ConvArgs &a, dim3 grid, size_t dyn, cudaStream_t s);

@@ -105,6 +105,8 @@ _SIGS = {
     "lsb_affine_nest": ([ctypes.POINTER(NestDesc), vp], ctypes.c_int),
     "lsb_launch_count": ([ctypes.c_int], ctypes.c_int64),
     "lsb_sizeof": ([ctypes.c_int], ctypes.c_int64),
+    "lsb_profile": ([ctypes.c_int], ctypes.c_int),
+    "lsb_last_kernel_ms": ([ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
 }
 
 #: ctypes mirrors of the lsb.h structs, in lsb_sizeof() order
@@ -163,6 +165,16 @@ def device_info(device: int = 0) -> dict:
     check(lib().lsb_device_info(device, ctypes.byref(sm), ctypes.byref(ma), ctypes.byref(mi),
                                 ctypes.byref(clk)), "lsb_device_info")
     return {"sm_count": sm.value, "cc": (ma.value, mi.value), "clock_khz": clk.value}
+
+
+def profile(enable: bool) -> None:
+    check(lib().lsb_profile(1 if enable else 0), "lsb_profile")
+
+
+def last_kernel_ms() -> float:
+    v = ctypes.c_float()
+    check(lib().lsb_last_kernel_ms(ctypes.byref(v)), "lsb_last_kernel_ms")
+    return float(v.value)
 
 
 def launch_count(reset: bool = False) -> int:
