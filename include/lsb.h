@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define LSB_ABI_VERSION 1
+#define LSB_ABI_VERSION 2
 
 /* reduce / combine operators: program.py:182 KIND_CODE */
 enum { LSB_OP_ADD = 0, LSB_OP_MUL = 1, LSB_OP_MAX = 2, LSB_OP_MIN = 3 };
@@ -104,7 +104,14 @@ typedef struct {
     int32_t tile_m, tile_n;    /* 0 = auto (split-factor hints)            */
     int64_t m_begin, m_end;    /* compute output rows [m_begin, m_end); m_end <= 0 -> M
                                   (row sharding across GPUs) */
+    int32_t flags;             /* LSB_GEMM_* bits                          */
+    int32_t reserved;
 } lsb_gemm_desc;
+
+/* lsb_gemm_desc.flags: B (pointer, extents, strides and contents) is the same
+ * as in the previous lsb_semiring_gemm call on this device -- the 3xTF32 path
+ * then reuses its hi/lo split of B (row-block streaming of one contraction) */
+#define LSB_GEMM_B_UNCHANGED 1
 
 /*
  * Direct 2-D convolution over NCHW-indexed tensors (any element strides),
@@ -179,6 +186,13 @@ int lsb_memcpy_h2d(void *dst, const void *src, size_t bytes, void *stream);
 int lsb_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream);
 int lsb_memcpy_d2d(void *dst, const void *src, size_t bytes, void *stream);
 int lsb_stream_sync(void *stream);
+/* streams / events for overlapping copies with kernels (row-block streaming) */
+int lsb_stream_create(void **stream);
+int lsb_stream_destroy(void *stream);
+int lsb_event_create(void **event);
+int lsb_event_destroy(void *event);
+int lsb_event_record(void *event, void *stream);
+int lsb_stream_wait_event(void *stream, void *event);
 
 /* ---- kernels ---------------------------------------------------------------- */
 int lsb_semiring_gemm(const lsb_gemm_desc *desc, void *stream);

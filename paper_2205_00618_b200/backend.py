@@ -290,6 +290,27 @@ class Runner:
             fn(d, stream)
         return native.launch_count() - before
 
+    def launch_rows(self, slots: dict[int, int], stream: int, r0: int, r1: int,
+                    b_unchanged: bool = False) -> int:
+        """Rows [r0, r1) of a single-GEMM plan (row-block streaming)."""
+        key = tuple(sorted(slots.items()))
+        if key != self._desc_key:
+            self._descs = self._build(slots)
+            self._desc_key = key
+        (fn, d), = self._descs
+        blk = native.GemmDesc()
+        ctypes.pointer(blk)[0] = d
+        blk.m_begin, blk.m_end = r0, r1
+        blk.flags = native.GEMM_B_UNCHANGED if b_unchanged else 0
+        before = native.launch_count()
+        fn(blk, stream)
+        return native.launch_count() - before
+
+    def streams(self):
+        if not hasattr(self, "_streams"):
+            self._streams = (native.Stream(), native.Stream(), native.Stream())
+        return self._streams
+
 
 def run_device(kernel: CompiledKernel, slots: dict[int, int], stream: int = 0) -> int:
     """Run on caller-owned device buffers (slot -> device pointer, e.g. torch
@@ -299,6 +320,87 @@ def run_device(kernel: CompiledKernel, slots: dict[int, int], stream: int = 0) -
     if missing:
         raise ShapeMismatch(f"slots {sorted(missing)} have no device buffer")
     return kernel.runner.launch(slots, stream)
+
+
+def _reads_c_in(plan: Plan) -> bool:
+    return any(e.c_in is not None for s in plan.steps for e in s.epi)
+
+
+#: row-block streaming kicks in from this many multiply-adds (one launch
+#: computes faster than its operands cross PCIe below it)
+STREAM_MIN_MACS = 1 << 34
+STREAM_BLOCKS = 8
+
+
+def _row_stream_plan(kernel: CompiledKernel, hosts: dict):
+    """Row blocks for copy/compute overlap, or None.  Applies to a plan that
+    is one batch-1 GEMM whose A rows and C rows are contiguous byte ranges of
+    their slots (M the slowest dim of both)."""
+    plan = kernel.plan
+    if len(plan.steps) != 1 or plan.steps[0].kind != "gemm":
+        return None
+    p = plan.steps[0].params
+    if p["batch"] != 1 or p["M"] < 2 * STREAM_BLOCKS * 128 or p["M"] * p["N"] * p["K"] < STREAM_MIN_MACS:
+        return None
+    (aref, abase), (cref, cbase) = p["A"], p["C"]
+    if aref.kind != "slot" or cref.kind != "slot" or abase or cbase:
+        return None
+    asize = int(np.prod(plan.slot_shapes[aref.key]))
+    csize = int(np.prod(plan.slot_shapes[cref.key]))
+    if p["sa_m"] * p["M"] != asize or p["sc_m"] * p["M"] != csize:
+        return None
+    if aref.key not in hosts:
+        return None
+    M = p["M"]
+    per = -(-M // STREAM_BLOCKS)
+    per = -(-per // 128) * 128
+    return [(r0, min(M, r0 + per)) for r0 in range(0, M, per)], aref.key, cref.key, p["sa_m"], p["sc_m"]
+
+
+def _execute_row_streamed(kernel, r: "Runner", dev, hosts, buffers, rows) -> int:
+    """H2D of A row-block i+1 and D2H of C row-block i-1 overlap the
+    contraction of block i (three streams; PCIe is full duplex).  B and the
+    other operands go up once; the 3xTF32 path splits B once
+    (LSB_GEMM_B_UNCHANGED on blocks after the first)."""
+    blocks, a_slot, c_slot, sa_m, sc_m = rows
+    s_in, s_c, s_out = r.streams()
+    pre = native.Event()
+    for slot, host in hosts.items():
+        if slot not in (a_slot, c_slot):
+            native.h2d(dev[slot], host.ctypes.data, host.nbytes, s_in.handle)
+    pre.record(s_in)
+    s_c.wait(pre)
+    ahost = hosts[a_slot]
+    chost_in = hosts.get(c_slot)       # C_in rows when the plan reads it
+    dst = buffers.get(c_slot)
+    direct = (dst is not None and dst.dtype == np.float32 and dst.flags.c_contiguous
+              and dst.flags.writeable)
+    out = dst if direct else np.empty(kernel.slot_shapes[c_slot], np.float32)
+    launches = 0
+    events = []
+    for i, (r0, r1) in enumerate(blocks):
+        ein, ec = native.Event(), native.Event()
+        native.h2d(dev[a_slot] + 4 * r0 * sa_m, ahost.ctypes.data + 4 * r0 * sa_m, 4 * (r1 - r0) * sa_m,
+                   s_in.handle)
+        if chost_in is not None:
+            native.h2d(dev[c_slot] + 4 * r0 * sc_m, chost_in.ctypes.data + 4 * r0 * sc_m,
+                       4 * (r1 - r0) * sc_m, s_in.handle)
+        ein.record(s_in)
+        s_c.wait(ein)
+        launches += r.launch_rows(dev, s_c.handle, r0, r1, b_unchanged=i > 0)
+        ec.record(s_c)
+        s_out.wait(ec)
+        native.d2h(out.ctypes.data + 4 * r0 * sc_m, dev[c_slot] + 4 * r0 * sc_m, 4 * (r1 - r0) * sc_m,
+                   s_out.handle)
+        events.append((ein, ec))
+    s_out.sync()
+    s_c.sync()
+    if not direct:
+        if dst is not None:
+            dst.reshape(-1)[:] = out.reshape(-1).astype(dst.dtype)
+        else:
+            buffers[c_slot] = out
+    return launches
 
 
 def execute(kernel: CompiledKernel, buffers: dict[int, np.ndarray]) -> None:
@@ -318,19 +420,25 @@ def execute(kernel: CompiledKernel, buffers: dict[int, np.ndarray]) -> None:
     dev = r.slot_buffers()
     stream = 0
     staged = []
+    hosts = {}
     for slot, arr in buffers.items():
-        if slot not in dev:
-            continue
-        host = np.ascontiguousarray(arr, dtype=np.float32)
+        if slot in dev:
+            hosts[slot] = np.ascontiguousarray(arr, dtype=np.float32)
+    reads_cin = _reads_c_in(kernel.plan)
+    for slot in kernel.output_slots:
+        if slot not in buffers and reads_cin:
+            # absent output read as C_in: zeros (the reference arena is np.zeros)
+            n = int(np.prod(kernel.slot_shapes[slot])) if kernel.slot_shapes[slot] else 1
+            hosts[slot] = np.zeros(n, np.float32)
+    rows = _row_stream_plan(kernel, hosts)
+    if rows is not None:
+        launches = _execute_row_streamed(kernel, r, dev, hosts, buffers, rows)
+        kernel.counters = {k: 0 for k in COUNTERS}
+        kernel.counters["launches"] = launches
+        return
+    for slot, host in hosts.items():
         staged.append(host)
         native.h2d(dev[slot], host.ctypes.data, host.nbytes, stream)
-    for slot in kernel.output_slots:
-        if slot not in buffers:
-            # absent output: C_in is zeros (reference arena is np.zeros)
-            n = int(np.prod(kernel.slot_shapes[slot])) if kernel.slot_shapes[slot] else 1
-            z = np.zeros(n, np.float32)
-            staged.append(z)
-            native.h2d(dev[slot], z.ctypes.data, z.nbytes, stream)
     launches = r.launch(dev, stream)
     outs = {}
     for slot in kernel.output_slots:

@@ -245,6 +245,32 @@ int lsb_stream_sync(void *stream) {
     LSB_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     return LSB_OK;
 }
+int lsb_stream_create(void **stream) {
+    if (!stream) return fail(LSB_ERR_INVALID, "null out");
+    LSB_CUDA(cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t *>(stream), cudaStreamNonBlocking));
+    return LSB_OK;
+}
+int lsb_stream_destroy(void *stream) {
+    LSB_CUDA(cudaStreamDestroy((cudaStream_t)stream));
+    return LSB_OK;
+}
+int lsb_event_create(void **event) {
+    if (!event) return fail(LSB_ERR_INVALID, "null out");
+    LSB_CUDA(cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t *>(event), cudaEventDisableTiming));
+    return LSB_OK;
+}
+int lsb_event_destroy(void *event) {
+    LSB_CUDA(cudaEventDestroy((cudaEvent_t)event));
+    return LSB_OK;
+}
+int lsb_event_record(void *event, void *stream) {
+    LSB_CUDA(cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream));
+    return LSB_OK;
+}
+int lsb_stream_wait_event(void *stream, void *event) {
+    LSB_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)event, 0));
+    return LSB_OK;
+}
 
 int lsb_profile(int enable) {
     if (enable && !g_prof_ev[0]) {
@@ -318,12 +344,14 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     if (algo < 0) return fail(LSB_ERR_UNSUPPORTED, "tf32x3 covers batch-1 (mul, add) contractions");
     if (algo == LSB_ALGO_TF32X3) {
         char err[256] = "";
+        int aux = 0;
         rc = lsb::tf32x3_gemm(M, d->N, d->K, a.A, d->sa_m, d->sa_k, d->B, d->sb_k, d->sb_n, a.C, d->sc_m,
-                              d->sc_n, a.c_vec, a.epi, s, err, sizeof(err));
+                              d->sc_n, a.c_vec, a.epi, (d->flags & LSB_GEMM_B_UNCHANGED) != 0, s, &aux,
+                              err, sizeof(err));
         if (rc) return fail(rc, "%s", err);
         rc = check_launch("tf32x3_gemm");
         if (rc) return rc;
-        g_launches.fetch_add(2, std::memory_order_relaxed);   // + the two split prepasses
+        g_launches.fetch_add(aux, std::memory_order_relaxed);   // + the split prepasses
         return LSB_OK;
     }
 

@@ -19,7 +19,7 @@ LSB_MAX_EPI = 4
 LSB_MAX_NEST_DIMS = 8
 LSB_MAX_NEST_OPERANDS = 4
 LSB_MAX_GUARDS = 4
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 i32, i64, f32, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
 
@@ -44,7 +44,11 @@ class GemmDesc(ctypes.Structure):
                 ("beta", f32), ("beta_in_loop", i32),
                 ("n_epi", i32), ("epi", EpiStage * LSB_MAX_EPI),
                 ("algo", i32), ("split_k", i32), ("tile_m", i32), ("tile_n", i32),
-                ("m_begin", i64), ("m_end", i64)]
+                ("m_begin", i64), ("m_end", i64),
+                ("flags", i32), ("reserved", i32)]
+
+
+GEMM_B_UNCHANGED = 1
 
 
 class ConvDesc(ctypes.Structure):
@@ -99,6 +103,12 @@ _SIGS = {
     "lsb_memcpy_d2h": ([vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
     "lsb_memcpy_d2d": ([vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
     "lsb_stream_sync": ([vp], ctypes.c_int),
+    "lsb_stream_create": ([ctypes.POINTER(vp)], ctypes.c_int),
+    "lsb_stream_destroy": ([vp], ctypes.c_int),
+    "lsb_event_create": ([ctypes.POINTER(vp)], ctypes.c_int),
+    "lsb_event_destroy": ([vp], ctypes.c_int),
+    "lsb_event_record": ([vp, vp], ctypes.c_int),
+    "lsb_stream_wait_event": ([vp, vp], ctypes.c_int),
     "lsb_semiring_gemm": ([ctypes.POINTER(GemmDesc), vp], ctypes.c_int),
     "lsb_gemm_algo": ([ctypes.POINTER(GemmDesc)], ctypes.c_int),
     "lsb_conv2d_nchw": ([ctypes.POINTER(ConvDesc), vp], ctypes.c_int),
@@ -241,6 +251,46 @@ def d2d(dst: int, src: int, nbytes: int, stream: int = 0) -> None:
 
 def sync(stream: int = 0) -> None:
     check(lib().lsb_stream_sync(vp(stream)), "lsb_stream_sync")
+
+
+class Stream:
+    """Non-blocking CUDA stream owned by the backend (copy/compute overlap)."""
+
+    def __init__(self):
+        p = vp()
+        check(lib().lsb_stream_create(ctypes.byref(p)), "lsb_stream_create")
+        self.handle = int(p.value)
+
+    def wait(self, event: "Event") -> None:
+        check(lib().lsb_stream_wait_event(vp(self.handle), vp(event.handle)), "lsb_stream_wait_event")
+
+    def sync(self) -> None:
+        sync(self.handle)
+
+    def __del__(self):
+        try:
+            if self.handle and _LIB is not None:
+                _LIB.lsb_stream_destroy(vp(self.handle))
+        except Exception:
+            pass
+
+
+class Event:
+    def __init__(self):
+        p = vp()
+        check(lib().lsb_event_create(ctypes.byref(p)), "lsb_event_create")
+        self.handle = int(p.value)
+
+    def record(self, stream: "Stream | int") -> None:
+        h = stream.handle if isinstance(stream, Stream) else int(stream)
+        check(lib().lsb_event_record(vp(self.handle), vp(h)), "lsb_event_record")
+
+    def __del__(self):
+        try:
+            if self.handle and _LIB is not None:
+                _LIB.lsb_event_destroy(vp(self.handle))
+        except Exception:
+            pass
 
 
 def semiring_gemm(desc: GemmDesc, stream: int = 0) -> None:
