@@ -43,13 +43,14 @@ bool load_encode() {
     return true;
 }
 
-bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp) {
+bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int bk) {
     cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)kp * sizeof(float)};
-    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)tc::BM};
+    cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)tc::BM};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box,
-                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -68,7 +69,11 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
         snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
         return LSB_ERR_UNSUPPORTED;
     }
-    const int64_t Kp = (K + tc::BK - 1) / tc::BK * tc::BK;
+    constexpr int kKAlign = 32;   // split buffers padded for either stage geometry
+    const int64_t Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
+    // long reductions stream 16 MiB operand blocks per tile: keep one CTA per
+    // SM (fewer concurrent streams through L2); otherwise two CTAs per SM
+    const int bk = K >= 8192 ? 32 : 16;
     const size_t need = sizeof(float) * (size_t)(2 * M + 2 * N) * (size_t)Kp;
     float *ws;
     bool reuse_b = false;
@@ -106,15 +111,17 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
         if (aux_launches) *aux_launches = reuse_b ? 1 : 2;
     }
     CUtensorMap mah, mal, mbh, mbl;
-    if (!make_map(&mah, ahi, M, Kp) || !make_map(&mal, alo, M, Kp) || !make_map(&mbh, bhi, N, Kp) ||
-        !make_map(&mbl, blo, N, Kp)) {
+    if (!make_map(&mah, ahi, M, Kp, bk) || !make_map(&mal, alo, M, Kp, bk) || !make_map(&mbh, bhi, N, Kp, bk) ||
+        !make_map(&mbl, blo, N, Kp, bk)) {
         snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
         return LSB_ERR_CUDA;
     }
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tc::tf32x3_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc::kSmemBytes);
+        cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc::Cfg<16>::kSmemBytes);
+        cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc::Cfg<32>::kSmemBytes);
         attr = true;
     }
     tc::TcArgs a;
@@ -126,7 +133,10 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     a.n_tiles = (int)((N + tc::BN - 1) / tc::BN);
     dim3 grid((unsigned)(a.m_tiles * a.n_tiles));
     prof_mark(0, s);
-    tc::tf32x3_gemm_kernel<<<grid, tc::kThreadsTC, tc::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
+    if (bk == 32)
+        tc::tf32x3_gemm_kernel<32><<<grid, tc::kThreadsTC, tc::Cfg<32>::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
+    else
+        tc::tf32x3_gemm_kernel<16><<<grid, tc::kThreadsTC, tc::Cfg<16>::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
     prof_mark(1, s);
     return LSB_OK;
 }

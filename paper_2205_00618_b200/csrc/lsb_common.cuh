@@ -56,16 +56,20 @@ __host__ __device__ __forceinline__ float identity_rt(int op) {
     }
 }
 
-// vm.py:214-228: relu = max(x, 0); sigmoid evaluated in f64 then rounded,
-// with the same two-branch formulation.
+// vm.py:214-228: sigmoid evaluated in f64 then rounded, with the same
+// two-branch formulation.  Out of line: inlining the f64 exp/div into every
+// epilogue element blew the tf32x3 kernel up to 15k SASS instructions.
+static __device__ __noinline__ float sigmoid_f64(float x) {
+    double d = (double)x;
+    if (d >= 0.0) return (float)(1.0 / (1.0 + exp(-d)));
+    double e = exp(d);
+    return (float)(e / (1.0 + e));
+}
+
+// vm.py:214-228: relu = max(x, 0)
 __device__ __forceinline__ float ew_rt(int ew, float x) {
     if (ew == LSB_EW_RELU) return fmaxf(x, 0.0f);
-    if (ew == LSB_EW_SIGMOID) {
-        double d = (double)x;
-        if (d >= 0.0) return (float)(1.0 / (1.0 + exp(-d)));
-        double e = exp(d);
-        return (float)(e / (1.0 + e));
-    }
+    if (ew == LSB_EW_SIGMOID) return sigmoid_f64(x);
     return x;
 }
 
@@ -78,8 +82,12 @@ struct EpiStages {
 // point, c0..c3 its coordinates in the kernel's output index space.
 __device__ __forceinline__ float apply_epilogue(const EpiStages &e, float x, int64_t c0,
                                                 int64_t c1, int64_t c2, int64_t c3) {
-#pragma unroll 1
-    for (int i = 0; i < e.n; i++) {
+    // fully unrolled over the static bound: e.s[i] must be a compile-time
+    // offset, or the whole stage table (kernel-parameter space) is copied to
+    // local memory for dynamic indexing (measured: 2.3x slower C4 epilogue)
+#pragma unroll
+    for (int i = 0; i < LSB_MAX_EPI; i++) {
+        if (i >= e.n) break;
         const lsb_epi_stage &st = e.s[i];
         float t = x;
         if (st.combine >= 0) {

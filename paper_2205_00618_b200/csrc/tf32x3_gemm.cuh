@@ -33,15 +33,27 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int BK = 32;                 // 32 fp32 = 128 B = one SWIZZLE_128B row
 constexpr int STAGES = 3;
-constexpr int kChunkK = 64;            // K per TMEM accumulation chunk (see below)
-constexpr int kChunkStages = kChunkK / BK;
+constexpr int kChunkK = 64;            // K per TMEM accumulation chunk (see header)
 constexpr int kThreadsTC = 192;
-constexpr int kTileBytes = BM * BK * 4;              // 16 KiB (A or B, hi or lo)
-constexpr int kStageBytes = 4 * kTileBytes;          // 64 KiB
-constexpr int kTmemCols = 2 * BN;                    // two chunk accumulators
-constexpr size_t kSmemBytes = (size_t)STAGES * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kTmemCols = 2 * BN;      // two chunk accumulators
+
+// Per-K-stage geometry.  BK = 16 (64 B rows, SWIZZLE_64B): ~97 KiB of smem,
+// two CTAs per SM, so one CTA's epilogue and prologue overlap the other's
+// MMAs (best for moderate K, e.g. C4).  BK = 32 (128 B rows, SWIZZLE_128B):
+// one CTA per SM, half as many CTAs streaming operands through L2 (best for
+// K = 16384, C5).  The launcher picks by K.
+template <int BK_>
+struct Cfg {
+    static constexpr int BK = BK_;
+    static constexpr int kSwizzleBytes = BK_ * 4;
+    static constexpr int kCtasPerSm = BK_ == 16 ? 2 : 1;
+    static constexpr int kChunkStages = kChunkK / BK_;
+    static constexpr int kTileBytes = BM * BK_ * 4;        // A or B, hi or lo
+    static constexpr int kStageBytes = 4 * kTileBytes;
+    static constexpr size_t kSmemBytes = (size_t)STAGES * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static_assert(STAGES * kStageBytes >= BM * BN * 4, "epilogue staging reuses the stage buffers");
+};
 
 constexpr int kGroupM = 16;            // tile raster: 16 m-tiles per group share B in L2
 
@@ -98,13 +110,14 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 
 // K-major operand tile in the canonical SWIZZLE_128B layout: rows of 128 B,
 // 8-row (1024 B) swizzle atoms stacked with SBO = 1024 B.
-__device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
+template <int kSwizzleBytes>
+__device__ __forceinline__ uint64_t sdesc_k_sw(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFFu);   // start address (16 B units)
     d |= (uint64_t)1 << 16;                    // leading byte offset (unused when swizzled)
-    d |= (uint64_t)(1024 >> 4) << 32;          // stride byte offset
+    d |= (uint64_t)((8 * kSwizzleBytes) >> 4) << 32;   // stride byte offset: 8-row atom
     d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;                    // layout: SWIZZLE_128B
+    d |= (uint64_t)(kSwizzleBytes == 128 ? 2 : 4) << 61;   // layout: SWIZZLE_128B / 64B
     return d;
 }
 
@@ -186,10 +199,14 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
 
 // ---------------------------------------------------------------- main kernel
 
-__global__ void __launch_bounds__(kThreadsTC, 1)
+template <int BK_>
+__global__ void __launch_bounds__(kThreadsTC, Cfg<BK_>::kCtasPerSm)
     tf32x3_gemm_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                        const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                        const TcArgs p) {
+    using Cf = Cfg<BK_>;
+    constexpr int BK = Cf::BK, kChunkStages = Cf::kChunkStages;
+    constexpr int kTileBytes = Cf::kTileBytes, kStageBytes = Cf::kStageBytes;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the SWIZZLE_128B atoms
     unsigned char *smem = reinterpret_cast<unsigned char *>(
@@ -279,9 +296,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t base = smem_u32(smem + stage * kStageBytes);
-                    const uint64_t ahi = sdesc_k_sw128(base), alo = sdesc_k_sw128(base + kTileBytes);
-                    const uint64_t bhi = sdesc_k_sw128(base + 2 * kTileBytes),
-                                   blo = sdesc_k_sw128(base + 3 * kTileBytes);
+                    const uint64_t ahi = sdesc_k_sw<Cf::kSwizzleBytes>(base), alo = sdesc_k_sw<Cf::kSwizzleBytes>(base + kTileBytes);
+                    const uint64_t bhi = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileBytes),
+                                   blo = sdesc_k_sw<Cf::kSwizzleBytes>(base + 3 * kTileBytes);
 #pragma unroll
                     for (int k = 0; k < BK / 8; k++) {
                         const uint64_t off = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along K
