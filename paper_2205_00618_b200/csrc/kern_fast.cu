@@ -17,6 +17,18 @@ GemmFn fast_gemm(int c, int r, int bm, bool two_level) {
     return nullptr;
 }
 
+// stream-K (add, max|min): identity fill of C, then the balanced kernel
+void launch_streamk(int reduce, const GemmArgs &a, int ctas, cudaStream_t s) {
+    const float id = reduce == LSB_OP_MAX ? -INFINITY : INFINITY;
+    const int64_t total = a.M * a.N;
+    const int fb = (int)std::min<int64_t>((total + 255) / 256, 2048);
+    fill_kernel<0><<<fb, 256, 0, s>>>(a.C, a.M, a.N, a.sc_m, a.sc_n, id);
+    if (reduce == LSB_OP_MAX)
+        semiring_streamk_kernel<LSB_OP_ADD, LSB_OP_MAX, 128><<<ctas, kThreads, 0, s>>>(a);
+    else
+        semiring_streamk_kernel<LSB_OP_ADD, LSB_OP_MIN, 128><<<ctas, kThreads, 0, s>>>(a);
+}
+
 void launch_conv_fast(const ConvArgs &a, dim3 grid, size_t dyn, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {

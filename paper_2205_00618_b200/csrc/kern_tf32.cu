@@ -141,4 +141,72 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     return LSB_OK;
 }
 
+// NCHW conv on the tensor cores: im2col+split prepass of the input (B, one
+// row per output pixel), gather+split of the filters (A, one row per output
+// channel), then the same 3xTF32 kernel in conv-output mode (m = co, n = pixel).
+int tf32x3_conv(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen) {
+    if (!load_encode()) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
+        return LSB_ERR_UNSUPPORTED;
+    }
+    const int64_t M = c.M, K = c.K, P = n_img * c.N;   // c.N = HO*WO pixels per image
+    const int64_t Kp = (K + 31) / 32 * 32;
+    const size_t need = sizeof(float) * (size_t)(2 * M + 2 * P) * (size_t)Kp;
+    float *ws;
+    {
+        std::lock_guard<std::mutex> lk(g_tc_mu);
+        if (need > g_split_bytes) {
+            if (g_split) {
+                cudaDeviceSynchronize();
+                cudaFree(g_split);
+                g_split = nullptr;
+                g_split_bytes = 0;
+            }
+            if (cudaMalloc(&g_split, need) != cudaSuccess) {
+                snprintf(err, errlen, "cudaMalloc(%zu) for the tf32 conv operands failed", need);
+                return LSB_ERR_NOMEM;
+            }
+            g_split_bytes = need;
+        }
+        g_bkey = BKey{};
+        ws = g_split;
+    }
+    float *bhi = ws, *blo = bhi + P * Kp, *ahi = blo + P * Kp, *alo = ahi + M * Kp;
+    tc::ConvGeom g;
+    g.C = c.C; g.H = c.H; g.W = c.W; g.R = c.R; g.S = c.S; g.HO = c.HO; g.WO = c.WO;
+    g.P = P; g.K = K; g.Kp = Kp;
+    g.sh = c.stride_h; g.sw = c.stride_w; g.ph = c.pad_h; g.pw = c.pad_w; g.dh = c.dil_h; g.dw = c.dil_w;
+    g.sx0 = c.sx0; g.sx1 = c.sx1; g.sx2 = c.sx2; g.sx3 = c.sx3;
+    g.fill = c.fill;
+    dim3 gi((unsigned)((Kp + 31) / 32), (unsigned)((P + 31) / 32));
+    tc::im2col_split_kernel<<<gi, 256, 0, s>>>(c.x, g, bhi, blo);
+    const int64_t wtot = M * Kp;
+    tc::filter_split_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
+        c.w, M, K, Kp, c.R, c.S, c.sw0, c.sw1, c.sw2, c.sw3, ahi, alo);
+    if (aux_launches) *aux_launches = 2;
+    const int bk = 16;
+    CUtensorMap mah, mal, mbh, mbl;
+    if (!make_map(&mah, ahi, M, Kp, bk) || !make_map(&mal, alo, M, Kp, bk) || !make_map(&mbh, bhi, P, Kp, bk) ||
+        !make_map(&mbl, blo, P, Kp, bk)) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
+        return LSB_ERR_CUDA;
+    }
+    cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tc::Cfg<16>::kSmemBytes);
+    tc::TcArgs a;
+    memset(&a, 0, sizeof(a));
+    a.M = M; a.N = P; a.K = K; a.Kp = Kp;
+    a.C = c.o;
+    a.conv_hw = c.HO * c.WO; a.conv_wo = c.WO;
+    a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
+    a.epi = c.epi;
+    a.m_tiles = (int)((M + tc::BM - 1) / tc::BM);
+    a.n_tiles = (int)((P + tc::BN - 1) / tc::BN);
+    dim3 grid((unsigned)(a.m_tiles * a.n_tiles));
+    prof_mark(0, s);
+    tc::tf32x3_gemm_kernel<16><<<grid, tc::kThreadsTC, tc::Cfg<16>::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
+    prof_mark(1, s);
+    return LSB_OK;
+}
+
 }  // namespace lsb

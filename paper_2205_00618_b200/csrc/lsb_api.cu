@@ -379,6 +379,26 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     const int64_t n_tiles = (d->N + lsb::kBN - 1) / lsb::kBN;
     const int64_t tiles = m_tiles * n_tiles * d->batch;
 
+    // (add, max|min) with no epilogue on a grid that would not fill a few
+    // waves: stream-K, exact atomic max/min merge (C2)
+    {
+        const int64_t slots = (int64_t)sm_count() * 2;
+        const int64_t t128 = ((M + 127) / 128) * n_tiles;
+        if (d->combine == LSB_OP_ADD && (d->reduce == LSB_OP_MAX || d->reduce == LSB_OP_MIN) &&
+            !d->beta_in_loop && d->beta == 1.0f && a.epi.n == 0 && d->batch == 1 && d->split_k == 0 &&
+            t128 < 3 * slots && d->K >= 64 * lsb::kBK && !getenv("LSB_NO_STREAMK")) {
+            const int64_t units = t128 * ((d->K + lsb::kBK - 1) / lsb::kBK);
+            const int ctas = (int)std::min<int64_t>(slots, std::max<int64_t>(1, units / 16));
+            lsb::prof_mark(0, s);
+            lsb::launch_streamk(d->reduce, a, ctas, s);
+            lsb::prof_mark(1, s);
+            rc = check_launch("semiring_streamk");
+            if (rc) return rc;
+            g_launches.fetch_add(1, std::memory_order_relaxed);   // + the identity fill
+            return LSB_OK;
+        }
+    }
+
     int splits = d->split_k;
     if (splits <= 0) {
         splits = 1;
@@ -450,6 +470,23 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     const bool wcontig = d->sw[3] == 1 && d->sw[2] == d->S && d->sw[1] == d->R * d->S;
     a.a_mode = (wcontig && aligned16(d->w) && d->sw[0] % 4 == 0 && K % 4 == 0) ? lsb::LD_VEC_K : lsb::LD_GENERIC;
 
+    // tensor-core path (materialised im2col + 3xTF32): opt-in only.  Measured
+    // on C3 the im2col/split prepass (8*P*K bytes) costs more than the SIMT
+    // implicit GEMM saves (0.185 ms vs 0.101 ms), so AUTO stays on SIMT.
+    bool use_tc = false;
+    if (const char *env = getenv("LSB_GEMM_ALGO")) {
+        if (!strcmp(env, "tf32x3")) use_tc = lsb::tf32x3_supported(a.M, a.N * d->N, K);
+    }
+    if (use_tc) {
+        char err[256] = "";
+        int aux = 0;
+        rc = lsb::tf32x3_conv(a, d->N, (cudaStream_t)stream, &aux, err, sizeof(err));
+        if (rc) return fail(rc, "%s", err);
+        rc = check_launch("tf32x3_conv");
+        if (rc) return rc;
+        g_launches.fetch_add(aux, std::memory_order_relaxed);
+        return LSB_OK;
+    }
     const int bm = 64;
     dim3 grid((unsigned)((a.N + lsb::kBN - 1) / lsb::kBN), (unsigned)((a.M + bm - 1) / bm), (unsigned)d->N);
     size_t dyn = (size_t)K * (sizeof(int64_t) + sizeof(int2));

@@ -19,6 +19,7 @@ void prof_mark(int which, cudaStream_t s);
 
 GemmFn fast_gemm(int combine, int reduce, int bm, bool two_level);   // kern_fast.cu (nullptr if untuned)
 void launch_conv_fast(const ConvArgs &a, dim3 grid, size_t dyn, cudaStream_t s);
+void launch_streamk(int reduce, const GemmArgs &a, int ctas, cudaStream_t s);   // 2 launches
 extern const GemmFn kGemmGeneric[4][4];          // kern_generic.cu
 extern const SplitFn kSplit[4];                  // kern_generic.cu
 extern const NestFn kNest[4][4];                 // kern_nest.cu
@@ -28,6 +29,7 @@ bool tf32x3_supported(int64_t M, int64_t N, int64_t K);
 int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, int64_t sa_k, const float *B,
                 int64_t sb_k, int64_t sb_n, float *C, int64_t sc_m, int64_t sc_n, int c_vec, const EpiStages &epi,
                 bool b_unchanged, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
+int tf32x3_conv(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
 
 template <int C, int R, bool B, int BM, bool TWO = false>
 void launch_gemm(const GemmArgs &a, dim3 grid, cudaStream_t s) {

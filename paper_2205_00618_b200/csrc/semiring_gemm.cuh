@@ -437,6 +437,107 @@ constexpr size_t gemm_dyn_smem() { return (size_t)(BM / 16) * 8 * kThreads * siz
 // grid: x = n tiles, y = m tiles * splits, z = batch
 // ---------------------------------------------------------------------------
 
+// reduction over [kbeg, kend) of one output tile into mk (smem double buffer
+// As/Bs; stage2 holds the two-level totals when TWO)
+template <int BM, bool TWO, class MK>
+__device__ __forceinline__ void mainloop(const GemmArgs &p, int64_t bz, int64_t m0, int64_t n0, int64_t kbeg,
+                                         int64_t kend, MK &mk, float (*As)[kBK][BM + 4], float (*Bs)[kBK][kBN],
+                                         float2 *stage2, int tx, int ty) {
+    constexpr int TM = BM / 16;
+    if (kbeg >= kend) return;
+    GemmLoader<BM> ld;
+    ld.load(p, bz, m0, n0, kbeg, kend);
+    ld.store(p, As[0], Bs[0]);
+    __syncthreads();
+    Frag<TM> f[2];
+    MK::frag(As[0][0], Bs[0][0], ty, tx, f[0]);
+    int buf = 0;
+    int chunk = 0;
+    for (int64_t k0 = kbeg; k0 < kend; k0 += kBK) {
+        const bool more = k0 + kBK < kend;
+        if (more) ld.load(p, bz, m0, n0, k0 + kBK, kend);
+        if (k0 + kBK <= kend) {
+            // barrier + next slice's first fragment, issued before the
+            // last k step of this slice so its latency overlaps the math
+            auto boundary = [&](Frag<TM> &nf) {
+                if (more) ld.store(p, As[buf ^ 1], Bs[buf ^ 1]);
+                __syncthreads();
+                if (more) MK::frag(As[buf ^ 1][0], Bs[buf ^ 1][0], ty, tx, nf);
+            };
+            mk.template full_slice<BM>(As[buf], Bs[buf], ty, tx, p.beta, f, boundary);
+        } else {
+            mk.template tail_slice<BM>(As[buf], Bs[buf], (int)(kend - k0), ty, tx, p.beta);
+        }
+        if constexpr (TWO) {
+            if (++chunk == kChunkSlices) {
+                mk.fold(stage2);
+                chunk = 0;
+            }
+        }
+        buf ^= 1;
+    }
+}
+
+// order-preserving float max/min through integer atomics (exact, so the
+// result does not depend on the order partial tiles arrive in)
+__device__ __forceinline__ void atomic_max_f32(float *a, float v) {
+    if (v >= 0.0f) atomicMax(reinterpret_cast<int *>(a), __float_as_int(v));
+    else atomicMin(reinterpret_cast<unsigned *>(a), __float_as_uint(v));
+}
+__device__ __forceinline__ void atomic_min_f32(float *a, float v) {
+    if (v >= 0.0f) atomicMin(reinterpret_cast<int *>(a), __float_as_int(v));
+    else atomicMax(reinterpret_cast<unsigned *>(a), __float_as_uint(v));
+}
+
+// Stream-K for (add, max|min) without epilogue: the tiles x k-slices work is
+// cut into gridDim.x equal contiguous ranges, so every SM slot gets the same
+// work however few tiles there are (C2: 64 tiles on 296 slots); partial tiles
+// merge with exact atomic max/min into C, pre-filled with the identity.
+template <int OPC, int OPR, int BM>
+__global__ void __launch_bounds__(kThreads, 2) semiring_streamk_kernel(const GemmArgs p) {
+    constexpr int TM = BM / 16;
+    __shared__ __align__(16) float As[2][kBK][BM + 4];
+    __shared__ __align__(16) float Bs[2][kBK][kBN];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + kBN - 1) / kBN;
+    const int64_t kslices = (p.K + kBK - 1) / kBK;
+    const int64_t units = m_tiles * n_tiles * kslices;
+    const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
+    using MK = Micro<OPC, OPR, false, TM>;
+    for (int64_t u = u0; u < u1;) {
+        const int64_t tile = u / kslices, ks = u % kslices;
+        const int64_t seg_end = min(u1, (tile + 1) * kslices);
+        const int64_t kbeg = ks * kBK, kend = min(p.K, (seg_end - tile * kslices) * kBK);
+        const int64_t m0 = (tile / n_tiles) * BM, n0 = (tile % n_tiles) * kBN;
+        MK mk;
+        mk.init();
+        __syncthreads();   // previous segment's readers are done with As/Bs
+        mainloop<BM, false>(p, 0, m0, n0, kbeg, kend, mk, As, Bs, nullptr, tx, ty);
+#pragma unroll
+        for (int i = 0; i < TM; i++) {
+            const int64_t m = m0 + row_of<TM>(ty, i);
+            if (m >= p.M) continue;
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int64_t n = n0 + col_of(tx, j);
+                if (n >= p.N) continue;
+                float *dst = p.C + m * p.sc_m + n * p.sc_n;
+                if constexpr (OPR == LSB_OP_MAX) atomic_max_f32(dst, mk.get(i, j));
+                else atomic_min_f32(dst, mk.get(i, j));
+            }
+        }
+        u = seg_end;
+    }
+}
+
+template <int kUnused = 0>
+__global__ void fill_kernel(float *C, int64_t M, int64_t N, int64_t sc_m, int64_t sc_n, float v) {
+    const int64_t total = M * N;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x)
+        C[(e / N) * sc_m + (e % N) * sc_n] = v;
+}
+
 template <int OPC, int OPR, bool BETA, int BM, bool TWO = false>
 __global__ void __launch_bounds__(kThreads, 2) semiring_gemm_kernel(const GemmArgs p) {
     constexpr int TM = BM / 16;
@@ -460,40 +561,7 @@ __global__ void __launch_bounds__(kThreads, 2) semiring_gemm_kernel(const GemmAr
         const float id = Op<OPR>::identity();
         for (int e = threadIdx.x; e < TM * 4 * kThreads; e += kThreads) stage2[e] = make_float2(id, id);
     }
-    GemmLoader<BM> ld;
-
-    if (kbeg < kend) {
-        ld.load(p, bz, m0, n0, kbeg, kend);
-        ld.store(p, As[0], Bs[0]);
-        __syncthreads();
-        Frag<TM> f[2];
-        MK::frag(As[0][0], Bs[0][0], ty, tx, f[0]);
-        int buf = 0;
-        int chunk = 0;
-        for (int64_t k0 = kbeg; k0 < kend; k0 += kBK) {
-            const bool more = k0 + kBK < kend;
-            if (more) ld.load(p, bz, m0, n0, k0 + kBK, kend);
-            if (k0 + kBK <= kend) {
-                // barrier + next slice's first fragment, issued before the
-                // last k step of this slice so its latency overlaps the math
-                auto boundary = [&](Frag<TM> &nf) {
-                    if (more) ld.store(p, As[buf ^ 1], Bs[buf ^ 1]);
-                    __syncthreads();
-                    if (more) MK::frag(As[buf ^ 1][0], Bs[buf ^ 1][0], ty, tx, nf);
-                };
-                mk.template full_slice<BM>(As[buf], Bs[buf], ty, tx, p.beta, f, boundary);
-            } else {
-                mk.template tail_slice<BM>(As[buf], Bs[buf], (int)(kend - k0), ty, tx, p.beta);
-            }
-            if constexpr (TWO) {
-                if (++chunk == kChunkSlices) {
-                    mk.fold(stage2);
-                    chunk = 0;
-                }
-            }
-            buf ^= 1;
-        }
-    }
+    mainloop<BM, TWO>(p, bz, m0, n0, kbeg, kend, mk, As, Bs, stage2, tx, ty);
     if constexpr (TWO) mk.unfold(stage2);
 
     // ---- epilogue

@@ -50,6 +50,29 @@ def test_small_case(case):
             assert np.array_equal(got[slot].reshape(vm[slot].shape), vm[slot]), "differs from VM"
 
 
+TC_CASES = [c for c in SMALL if c["name"] in (
+    "semiring_mul_add", "fma_node", "transposed_gemm", "kat_identity_operand", "kat_alpha1_beta0",
+    "epi_beta_half_mul_add", "epi_beta_neg_mul_add", "epi_alpha_relu_pre_mul_add",
+    "epi_alpha_sig_post_mul_add", "epi_post_relu_mul_add", "mlp_bias_relu_small",
+    "mlp_alpha_relu_small", "mlp_bias_sigmoid_small", "acc_mm16", "acc_mm64",
+    "conv_valid_small", "conv_pad1_small", "conv_stride2_small")]
+
+
+@pytest.mark.parametrize("case", TC_CASES, ids=[c["name"] for c in TC_CASES])
+def test_small_case_forced_tensor_core_path(case, monkeypatch):
+    """The same fixtures through the 3xTF32 tcgen05 kernels (GEMM and
+    im2col conv), which auto-selection only uses for large problems."""
+    monkeypatch.setenv("LSB_GEMM_ALGO", "tf32x3")
+    gj = common.graph_json(case["graph"])
+    ins, ref, _ = common.case_data(case)
+    k, got = _run(gj, ins)
+    for slot, r in ref.items():
+        m = common.ref_metric(got[slot], r)
+        assert m <= 1e-4, f"{case['name']}: metric {m}"
+        if case["rule"] in ("tol", "exact"):
+            assert common.strict_ok(got[slot], r).all(), case["name"]
+
+
 def test_inputs_not_mutated_and_output_inserted():
     case = next(c for c in SMALL if c["name"] == "semiring_mul_add")
     ins, ref, _ = common.case_data(case)
