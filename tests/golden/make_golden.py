@@ -247,7 +247,7 @@ def main():
     # same ops under random legal schedules (schedule invariance)
     rng = random.Random(2024)
     for name, build in op_graphs.ACCEPTANCE_OPS.items():
-        for j in range(3):
+        for j in range(20):
             dfg = build()
             random_actions(dfg, rng, max_splits=3)
             small_case(f"fuzz_{name}_{j}", dfg, int_inputs(dfg, 500 + j), "exact", vm=False,
