@@ -43,16 +43,68 @@ bool load_encode() {
     return true;
 }
 
-bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int bk) {
+bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int bk, int box_rows) {
     cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)kp * sizeof(float)};
-    cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)tc::BM};
+    cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box,
                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                           bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+// tensor maps + launch of the main kernel for one tile geometry; A rows are
+// output rows (m), B rows output columns (n), both K-major [rows][Kp]
+template <int BK, int BN>
+int run_main(const float *ahi, const float *alo, const float *bhi, const float *blo, int64_t m_rows,
+             int64_t n_rows, int64_t Kp, tc::TcArgs a, cudaStream_t s, char *err, size_t errlen) {
+    using Cf = tc::Cfg<BK, BN>;
+    CUtensorMap mah, mal, mbh, mbl;
+    if (!make_map(&mah, ahi, m_rows, Kp, BK, tc::BM) || !make_map(&mal, alo, m_rows, Kp, BK, tc::BM) ||
+        !make_map(&mbh, bhi, n_rows, Kp, BK, BN) || !make_map(&mbl, blo, n_rows, Kp, BK, BN)) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
+        return LSB_ERR_CUDA;
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<BK, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Cf::kSmemBytes);
+        attr = true;
+    }
+    a.m_tiles = (int)((m_rows + tc::BM - 1) / tc::BM);
+    a.n_tiles = (int)((n_rows + BN - 1) / BN);
+    dim3 grid((unsigned)(a.m_tiles * a.n_tiles));
+    prof_mark(0, s);
+    tc::tf32x3_gemm_kernel<BK, BN><<<grid, Cf::kThreads, Cf::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
+    prof_mark(1, s);
+    return LSB_OK;
+}
+
+// tile geometry: LSB_TC_CFG=16x128|32x128|16x256 overrides (experiments)
+// measured (profiles/r01_tf32x3_cfg.log, TFLOP/s):
+//                      16x128  32x128  16x256
+//   4096x4096x1024      161     156     178
+//   8192^3              213     207     245
+//   16384^3             156     165     219
+// With a fused elementwise epilogue and short K the epilogue is a large share
+// of a tile, and only the 2-CTA/SM geometry hides it (C4: 113 vs 107 TF/s).
+int pick_cfg(int64_t N, int64_t K, bool has_epi) {
+    if (const char *e = getenv("LSB_TC_CFG")) {
+        if (!strcmp(e, "16x128")) return 0;
+        if (!strcmp(e, "32x128")) return 1;
+        if (!strcmp(e, "16x256")) return 2;
+    }
+    if (has_epi && K < 4096) return 0;
+    return N >= 256 ? 2 : 0;
+}
+
+int run_main_cfg(int cfg, const float *ahi, const float *alo, const float *bhi, const float *blo, int64_t m_rows,
+                 int64_t n_rows, int64_t Kp, const tc::TcArgs &a, cudaStream_t s, char *err, size_t errlen) {
+    if (cfg == 1) return run_main<32, 128>(ahi, alo, bhi, blo, m_rows, n_rows, Kp, a, s, err, errlen);
+    if (cfg == 2) return run_main<16, 256>(ahi, alo, bhi, blo, m_rows, n_rows, Kp, a, s, err, errlen);
+    return run_main<16, 128>(ahi, alo, bhi, blo, m_rows, n_rows, Kp, a, s, err, errlen);
 }
 
 }  // namespace
@@ -71,9 +123,6 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     }
     constexpr int kKAlign = 32;   // split buffers padded for either stage geometry
     const int64_t Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
-    // long reductions stream 16 MiB operand blocks per tile: keep one CTA per
-    // SM (fewer concurrent streams through L2); otherwise two CTAs per SM
-    const int bk = K >= 8192 ? 32 : 16;
     const size_t need = sizeof(float) * (size_t)(2 * M + 2 * N) * (size_t)Kp;
     float *ws;
     bool reuse_b = false;
@@ -110,35 +159,12 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
         }
         if (aux_launches) *aux_launches = reuse_b ? 1 : 2;
     }
-    CUtensorMap mah, mal, mbh, mbl;
-    if (!make_map(&mah, ahi, M, Kp, bk) || !make_map(&mal, alo, M, Kp, bk) || !make_map(&mbh, bhi, N, Kp, bk) ||
-        !make_map(&mbl, blo, N, Kp, bk)) {
-        snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
-        return LSB_ERR_CUDA;
-    }
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc::Cfg<16>::kSmemBytes);
-        cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc::Cfg<32>::kSmemBytes);
-        attr = true;
-    }
     tc::TcArgs a;
     memset(&a, 0, sizeof(a));
     a.M = M; a.N = N; a.K = K; a.Kp = Kp;
     a.C = C; a.sc_m = sc_m; a.sc_n = sc_n; a.c_vec = c_vec;
     a.epi = epi;
-    a.m_tiles = (int)((M + tc::BM - 1) / tc::BM);
-    a.n_tiles = (int)((N + tc::BN - 1) / tc::BN);
-    dim3 grid((unsigned)(a.m_tiles * a.n_tiles));
-    prof_mark(0, s);
-    if (bk == 32)
-        tc::tf32x3_gemm_kernel<32><<<grid, tc::kThreadsTC, tc::Cfg<32>::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
-    else
-        tc::tf32x3_gemm_kernel<16><<<grid, tc::kThreadsTC, tc::Cfg<16>::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
-    prof_mark(1, s);
-    return LSB_OK;
+    return run_main_cfg(pick_cfg(N, K, epi.n > 0), ahi, alo, bhi, blo, M, N, Kp, a, s, err, errlen);
 }
 
 // NCHW conv on the tensor cores: im2col+split prepass of the input (B, one
@@ -184,15 +210,6 @@ int tf32x3_conv(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launc
     tc::filter_split_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
         c.w, M, K, Kp, c.R, c.S, c.sw0, c.sw1, c.sw2, c.sw3, ahi, alo);
     if (aux_launches) *aux_launches = 2;
-    const int bk = 16;
-    CUtensorMap mah, mal, mbh, mbl;
-    if (!make_map(&mah, ahi, M, Kp, bk) || !make_map(&mal, alo, M, Kp, bk) || !make_map(&mbh, bhi, P, Kp, bk) ||
-        !make_map(&mbl, blo, P, Kp, bk)) {
-        snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
-        return LSB_ERR_CUDA;
-    }
-    cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)tc::Cfg<16>::kSmemBytes);
     tc::TcArgs a;
     memset(&a, 0, sizeof(a));
     a.M = M; a.N = P; a.K = K; a.Kp = Kp;
@@ -200,13 +217,7 @@ int tf32x3_conv(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launc
     a.conv_hw = c.HO * c.WO; a.conv_wo = c.WO;
     a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
     a.epi = c.epi;
-    a.m_tiles = (int)((M + tc::BM - 1) / tc::BM);
-    a.n_tiles = (int)((P + tc::BN - 1) / tc::BN);
-    dim3 grid((unsigned)(a.m_tiles * a.n_tiles));
-    prof_mark(0, s);
-    tc::tf32x3_gemm_kernel<16><<<grid, tc::kThreadsTC, tc::Cfg<16>::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
-    prof_mark(1, s);
-    return LSB_OK;
+    return run_main_cfg(0, ahi, alo, bhi, blo, M, P, Kp, a, s, err, errlen);
 }
 
 }  // namespace lsb

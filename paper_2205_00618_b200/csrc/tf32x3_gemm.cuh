@@ -32,27 +32,31 @@ namespace lsb {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BN = 128;
-constexpr int STAGES = 3;
 constexpr int kChunkK = 64;            // K per TMEM accumulation chunk (see header)
-constexpr int kThreadsTC = 192;
-constexpr int kTmemCols = 2 * BN;      // two chunk accumulators
 
-// Per-K-stage geometry.  BK = 16 (64 B rows, SWIZZLE_64B): ~97 KiB of smem,
-// two CTAs per SM, so one CTA's epilogue and prologue overlap the other's
-// MMAs (best for moderate K, e.g. C4).  BK = 32 (128 B rows, SWIZZLE_128B):
-// one CTA per SM, half as many CTAs streaming operands through L2 (best for
-// K = 16384, C5).  The launcher picks by K.
-template <int BK_>
+// Tile / stage geometry (the launcher picks by shape):
+//   <16, 128>  64-B K rows (SWIZZLE_64B), 3 stages, ~97 KiB: two CTAs per SM,
+//              one CTA's epilogue/prologue overlaps the other's MMAs (moderate K)
+//   <32, 128>  128-B K rows (SWIZZLE_128B), 3 stages, one CTA per SM
+//   <16, 256>  128x256 tiles (UMMA N = 256), 4 stages, one CTA per SM, eight
+//              epilogue warps: 25 % fewer operand bytes per flop (long K, C5)
+template <int BK_, int BN_>
 struct Cfg {
     static constexpr int BK = BK_;
+    static constexpr int BN = BN_;
     static constexpr int kSwizzleBytes = BK_ * 4;
-    static constexpr int kCtasPerSm = BK_ == 16 ? 2 : 1;
+    static constexpr int STAGES = BN_ == 256 ? 4 : 3;
+    static constexpr int kCtasPerSm = (BK_ == 16 && BN_ == 128) ? 2 : 1;
+    static constexpr int kEpiWarps = BN_ / 32;
+    static constexpr int kThreads = 64 + 32 * kEpiWarps;
     static constexpr int kChunkStages = kChunkK / BK_;
-    static constexpr int kTileBytes = BM * BK_ * 4;        // A or B, hi or lo
-    static constexpr int kStageBytes = 4 * kTileBytes;
+    static constexpr int kTileA = BM * BK_ * 4;            // A hi or lo
+    static constexpr int kTileB = BN_ * BK_ * 4;           // B hi or lo
+    static constexpr int kStageBytes = 2 * (kTileA + kTileB);
+    static constexpr int kTmemCols = 2 * BN_;              // two chunk accumulators
     static constexpr size_t kSmemBytes = (size_t)STAGES * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-    static_assert(STAGES * kStageBytes >= BM * BN * 4, "epilogue staging reuses the stage buffers");
+    static_assert(STAGES * kStageBytes >= BM * BN_ * 4, "epilogue staging reuses the stage buffers");
+    static_assert(kTmemCols <= 512, "TMEM has 512 columns");
 };
 
 constexpr int kGroupM = 16;            // tile raster: 16 m-tiles per group share B in L2
@@ -276,16 +280,17 @@ __global__ void __launch_bounds__(256) filter_split_kernel(const float *__restri
 
 // ---------------------------------------------------------------- main kernel
 
-template <int BK_>
-__global__ void __launch_bounds__(kThreadsTC, Cfg<BK_>::kCtasPerSm)
+template <int BK_, int BN_>
+__global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasPerSm)
     tf32x3_gemm_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                        const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                        const TcArgs p) {
-    using Cf = Cfg<BK_>;
-    constexpr int BK = Cf::BK, kChunkStages = Cf::kChunkStages;
-    constexpr int kTileBytes = Cf::kTileBytes, kStageBytes = Cf::kStageBytes;
+    using Cf = Cfg<BK_, BN_>;
+    constexpr int BK = Cf::BK, BN = Cf::BN, STAGES = Cf::STAGES, kChunkStages = Cf::kChunkStages;
+    constexpr int kTileA = Cf::kTileA, kTileB = Cf::kTileB, kStageBytes = Cf::kStageBytes;
+    constexpr int kEpiWarps = Cf::kEpiWarps;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte alignment for the SWIZZLE_128B atoms
+    // 1024-byte alignment for the swizzle atoms
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * kStageBytes);
@@ -322,13 +327,13 @@ __global__ void __launch_bounds__(kThreadsTC, Cfg<BK_>::kCtasPerSm)
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);   // one arrive per epilogue warp
+            mbar_init(&tempty[b], kEpiWarps);   // one arrive per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kTmemCols));
+                     "r"(Cf::kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -347,9 +352,9 @@ __global__ void __launch_bounds__(kThreadsTC, Cfg<BK_>::kCtasPerSm)
                 mbar_expect_tx(&full[stage], kStageBytes);
                 const int kx = kb * BK;
                 tma_load_2d(&map_ahi, &full[stage], base, kx, (int)m0);
-                tma_load_2d(&map_alo, &full[stage], base + kTileBytes, kx, (int)m0);
-                tma_load_2d(&map_bhi, &full[stage], base + 2 * kTileBytes, kx, (int)n0);
-                tma_load_2d(&map_blo, &full[stage], base + 3 * kTileBytes, kx, (int)n0);
+                tma_load_2d(&map_alo, &full[stage], base + kTileA, kx, (int)m0);
+                tma_load_2d(&map_bhi, &full[stage], base + 2 * kTileA, kx, (int)n0);
+                tma_load_2d(&map_blo, &full[stage], base + 2 * kTileA + kTileB, kx, (int)n0);
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -373,9 +378,10 @@ __global__ void __launch_bounds__(kThreadsTC, Cfg<BK_>::kCtasPerSm)
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t base = smem_u32(smem + stage * kStageBytes);
-                    const uint64_t ahi = sdesc_k_sw<Cf::kSwizzleBytes>(base), alo = sdesc_k_sw<Cf::kSwizzleBytes>(base + kTileBytes);
-                    const uint64_t bhi = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileBytes),
-                                   blo = sdesc_k_sw<Cf::kSwizzleBytes>(base + 3 * kTileBytes);
+                    const uint64_t ahi = sdesc_k_sw<Cf::kSwizzleBytes>(base);
+                    const uint64_t alo = sdesc_k_sw<Cf::kSwizzleBytes>(base + kTileA);
+                    const uint64_t bhi = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileA);
+                    const uint64_t blo = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileA + kTileB);
 #pragma unroll
                     for (int k = 0; k < BK / 8; k++) {
                         const uint64_t off = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along K
@@ -394,20 +400,22 @@ __global__ void __launch_bounds__(kThreadsTC, Cfg<BK_>::kCtasPerSm)
             }
         }
     } else {
-        // ---------------- epilogue warps 2..5
-        const int q = warp & 3;                   // TMEM lane quadrant of this warp
+        // ---------------- epilogue warps: warp w reads TMEM lane quadrant
+        // w % 4 and column half (w - 2) / 4 (BN = 256 uses 8 warps)
+        const int q = warp & 3;
+        const int ch = (warp - 2) >> 2;           // 128-column half of the tile
         const int row = q * 32 + lane;
-        float tot[BN];
+        float tot[128];
 #pragma unroll
-        for (int i = 0; i < BN; i++) tot[i] = 0.0f;
+        for (int i = 0; i < 128; i++) tot[i] = 0.0f;
         for (int c = 0; c < num_chunks; c++) {
             const int b = c & 1;
             mbar_wait(&tfull[b], (uint32_t)((c >> 1) & 1));
             tc_fence_after();
 #pragma unroll
-            for (int part = 0; part < BN / 32; part++) {
+            for (int part = 0; part < 4; part++) {
                 float v[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + part * 32), v);
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + ch * 128 + part * 32), v);
 #pragma unroll
                 for (int i = 0; i < 32; i++) tot[part * 32 + i] += v[i];
             }
@@ -421,46 +429,52 @@ __global__ void __launch_bounds__(kThreadsTC, Cfg<BK_>::kCtasPerSm)
         // every TMA load was consumed by an MMA whose completion preceded the
         // last tfull arrive, so the stage buffers are free
 #pragma unroll
-        for (int ch = 0; ch < BN / 4; ch++) {
-            const int pos = ch ^ (row & 31);
+        for (int c4 = 0; c4 < 32; c4++) {
+            const int chunk = ch * 32 + c4;
+            const int pos = chunk ^ (row & 31);
             *reinterpret_cast<float4 *>(tile + row * BN + pos * 4) =
-                make_float4(tot[ch * 4], tot[ch * 4 + 1], tot[ch * 4 + 2], tot[ch * 4 + 3]);
+                make_float4(tot[c4 * 4], tot[c4 * 4 + 1], tot[c4 * 4 + 2], tot[c4 * 4 + 3]);
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");   // epilogue warps only
-        const int ew = warp - 2;                          // 0..3, 32 rows each
+        asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");   // epilogue warps only
+        const int ew = warp - 2;
+        constexpr int kRowsPerWarp = BM / kEpiWarps;
 #pragma unroll 1
-        for (int rr = 0; rr < 32; rr++) {
-            const int r = ew * 32 + rr;
+        for (int rr = 0; rr < kRowsPerWarp; rr++) {
+            const int r = ew * kRowsPerWarp + rr;
             const int64_t m = m0 + r;
             if (m >= p.M) continue;
-            const int pos = lane ^ (r & 31);
-            float4 v = *reinterpret_cast<const float4 *>(tile + r * BN + pos * 4);
-            const int64_t n = n0 + lane * 4;
-            float x[4] = {v.x, v.y, v.z, v.w};
-            if (p.conv_hw > 0) {
 #pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    const int64_t pix = n + e;
-                    if (pix >= p.N) continue;
-                    const int64_t img = pix / p.conv_hw, hw = pix % p.conv_hw;
-                    const int64_t ho = hw / p.conv_wo, wo = hw % p.conv_wo;
-                    float y = x[e];
-                    if (p.epi.n) y = apply_epilogue(p.epi, y, img, m, ho, wo);
-                    p.C[img * p.so[0] + m * p.so[1] + ho * p.so[2] + wo * p.so[3]] = y;
+            for (int h = 0; h < BN / 128; h++) {
+                const int chunk = h * 32 + lane;
+                const int pos = chunk ^ (r & 31);
+                float4 v = *reinterpret_cast<const float4 *>(tile + r * BN + pos * 4);
+                const int64_t n = n0 + chunk * 4;
+                float x[4] = {v.x, v.y, v.z, v.w};
+                if (p.conv_hw > 0) {
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int64_t pix = n + e;
+                        if (pix >= p.N) continue;
+                        const int64_t img = pix / p.conv_hw, hw = pix % p.conv_hw;
+                        const int64_t ho = hw / p.conv_wo, wo = hw % p.conv_wo;
+                        float y = x[e];
+                        if (p.epi.n) y = apply_epilogue(p.epi, y, img, m, ho, wo);
+                        p.C[img * p.so[0] + m * p.so[1] + ho * p.so[2] + wo * p.so[3]] = y;
+                    }
+                    continue;
                 }
-                continue;
-            }
-            if (p.epi.n) {
+                if (p.epi.n) {
 #pragma unroll
-                for (int e = 0; e < 4; e++) x[e] = apply_epilogue(p.epi, x[e], 0, m, n + e, 0);
-            }
-            float *dst = p.C + m * p.sc_m;
-            if (p.c_vec && n + 3 < p.N) {
-                *reinterpret_cast<float4 *>(dst + n) = make_float4(x[0], x[1], x[2], x[3]);
-            } else {
+                    for (int e = 0; e < 4; e++) x[e] = apply_epilogue(p.epi, x[e], 0, m, n + e, 0);
+                }
+                float *dst = p.C + m * p.sc_m;
+                if (p.c_vec && n + 3 < p.N) {
+                    *reinterpret_cast<float4 *>(dst + n) = make_float4(x[0], x[1], x[2], x[3]);
+                } else {
 #pragma unroll
-                for (int e = 0; e < 4; e++)
-                    if (n + e < p.N) dst[(n + e) * p.sc_n] = x[e];
+                    for (int e = 0; e < 4; e++)
+                        if (n + e < p.N) dst[(n + e) * p.sc_n] = x[e];
+                }
             }
         }
     }
@@ -468,7 +482,7 @@ __global__ void __launch_bounds__(kThreadsTC, Cfg<BK_>::kCtasPerSm)
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::kTmemCols));
     }
 }
 
