@@ -29,6 +29,12 @@ void launch_streamk(int reduce, const GemmArgs &a, int ctas, cudaStream_t s) {
         semiring_streamk_kernel<LSB_OP_ADD, LSB_OP_MIN, 128><<<ctas, kThreads, 0, s>>>(a);
 }
 
+void launch_conv_fold(const ConvArgs &a, int64_t n_img, cudaStream_t s) {
+    const int64_t total = n_img * a.M * a.N;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
+    conv_splitk_fold_kernel<0><<<blocks, 256, 0, s>>>(a, n_img);
+}
+
 void launch_conv_fast(const ConvArgs &a, dim3 grid, size_t dyn, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {

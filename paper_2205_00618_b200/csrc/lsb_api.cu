@@ -488,12 +488,44 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
         return LSB_OK;
     }
     const int bm = 64;
-    dim3 grid((unsigned)((a.N + lsb::kBN - 1) / lsb::kBN), (unsigned)((a.M + bm - 1) / bm), (unsigned)d->N);
+    const int64_t m_tiles = (a.M + bm - 1) / bm;
+    const int64_t tiles = ((a.N + lsb::kBN - 1) / lsb::kBN) * m_tiles * d->N;
+    // split the (c, r, s) taps when the tiles underfill the 2-CTA/SM slots
+    // (C3: 200 tiles for 296 slots); same wave cost model as the GEMM split-K
+    int splits = 1;
+    {
+        const int64_t slots = (int64_t)sm_count() * 2;
+        const int64_t k_slices = (K + lsb::kBK - 1) / lsb::kBK;
+        if (tiles < 2 * slots && k_slices >= 16 && !getenv("LSB_NO_CONV_SPLIT")) {
+            // cost = the busiest SM's CTA count x work per CTA (+ fold traffic)
+            const int64_t sms = sm_count();
+            double best = 1e30;
+            for (int s = 1; s <= 8 && s <= k_slices / 8; s++) {
+                const int64_t per_sm = (tiles * s + sms - 1) / sms;
+                const double cost = (double)per_sm / s + 0.05 * (s > 1 ? s : 0);
+                if (cost < best - 1e-9) { best = cost; splits = s; }
+            }
+        }
+        if (const char *e = getenv("LSB_CONV_SPLITS")) splits = std::max(1, atoi(e));
+    }
+    int64_t kps = (K + splits - 1) / splits;
+    kps = (kps + lsb::kBK - 1) / lsb::kBK * lsb::kBK;
+    splits = (int)((K + kps - 1) / kps);
+    a.k_per_split = kps;
+    a.splits = splits;
+    if (splits > 1) {
+        rc = workspace(sizeof(float) * (size_t)splits * d->N * a.M * a.N, &a.ws);
+        if (rc) return rc;
+    }
+    dim3 grid((unsigned)((a.N + lsb::kBN - 1) / lsb::kBN), (unsigned)(m_tiles * splits), (unsigned)d->N);
     size_t dyn = (size_t)K * (sizeof(int64_t) + sizeof(int2));
     lsb::prof_mark(0, (cudaStream_t)stream);
     lsb::launch_conv_fast(a, grid, dyn, (cudaStream_t)stream);
     lsb::prof_mark(1, (cudaStream_t)stream);
-    return check_launch("conv_igemm");
+    rc = check_launch("conv_igemm");
+    if (rc || splits == 1) return rc;
+    lsb::launch_conv_fold(a, d->N, (cudaStream_t)stream);
+    return check_launch("conv_splitk_fold");
 }
 
 int lsb_affine_nest(const lsb_nest_desc *d, void *stream) {

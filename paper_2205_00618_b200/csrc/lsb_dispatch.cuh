@@ -19,6 +19,7 @@ void prof_mark(int which, cudaStream_t s);
 
 GemmFn fast_gemm(int combine, int reduce, int bm, bool two_level);   // kern_fast.cu (nullptr if untuned)
 void launch_conv_fast(const ConvArgs &a, dim3 grid, size_t dyn, cudaStream_t s);
+void launch_conv_fold(const ConvArgs &a, int64_t n_img, cudaStream_t s);
 void launch_streamk(int reduce, const GemmArgs &a, int ctas, cudaStream_t s);   // 2 launches
 extern const GemmFn kGemmGeneric[4][4];          // kern_generic.cu
 extern const SplitFn kSplit[4];                  // kern_generic.cu

@@ -59,6 +59,9 @@ struct ConvArgs {
     float *o; int64_t so0, so1, so2, so3;
     int a_mode;            // LD_VEC_K when filters are (c,r,s)-contiguous
     float beta;
+    int64_t k_per_split;   // split-K over the (c, r, s) taps (grid y = co tiles * splits)
+    int splits;
+    float *ws;             // partials [splits][img][co][pixel] or null
     EpiStages epi;
 };
 
@@ -659,9 +662,13 @@ __global__ void __launch_bounds__(kThreads, 2) conv_igemm_kernel(const ConvArgs 
     int2 *krs = reinterpret_cast<int2 *>(dyn + sizeof(int64_t) * p.K);
 
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int64_t m0 = (int64_t)blockIdx.y * BM;
+    const int64_t m_tiles = (p.M + BM - 1) / BM;
+    const int64_t split = blockIdx.y / m_tiles;
+    const int64_t m0 = (blockIdx.y % m_tiles) * BM;
     const int64_t n0 = (int64_t)blockIdx.x * kBN;
     const int64_t img = blockIdx.z;
+    const int64_t kbeg = split * p.k_per_split;
+    const int64_t kend = min(p.K, kbeg + p.k_per_split);
     const int64_t rs = p.R * p.S;
     for (int64_t k = threadIdx.x; k < p.K; k += kThreads) {
         int64_t ci = k / rs, r = (k % rs) / p.S, s = k % p.S;
@@ -676,16 +683,16 @@ __global__ void __launch_bounds__(kThreads, 2) conv_igemm_kernel(const ConvArgs 
     using MK = Micro<OPC, OPR, BETA, TM>;
     MK mk;
     mk.init();
-    ld.load<BM>(p, koff, krs, m0, 0, p.K);
+    ld.load<BM>(p, koff, krs, m0, kbeg, kend);
     ld.store<BM>(p, As[0], Bs[0]);
     __syncthreads();
     Frag<TM> f[2];
     MK::frag(As[0][0], Bs[0][0], ty, tx, f[0]);
     int buf = 0;
-    for (int64_t k0 = 0; k0 < p.K; k0 += kBK) {
-        const bool more = k0 + kBK < p.K;
-        if (more) ld.load<BM>(p, koff, krs, m0, k0 + kBK, p.K);
-        if (k0 + kBK <= p.K) {
+    for (int64_t k0 = kbeg; k0 < kend; k0 += kBK) {
+        const bool more = k0 + kBK < kend;
+        if (more) ld.load<BM>(p, koff, krs, m0, k0 + kBK, kend);
+        if (k0 + kBK <= kend) {
             auto boundary = [&](Frag<TM> &nf) {
                 if (more) ld.store<BM>(p, As[buf ^ 1], Bs[buf ^ 1]);
                 __syncthreads();
@@ -693,9 +700,32 @@ __global__ void __launch_bounds__(kThreads, 2) conv_igemm_kernel(const ConvArgs 
             };
             mk.template full_slice<BM>(As[buf], Bs[buf], ty, tx, p.beta, f, boundary);
         } else {
-            mk.template tail_slice<BM>(As[buf], Bs[buf], (int)(p.K - k0), ty, tx, p.beta);
+            mk.template tail_slice<BM>(As[buf], Bs[buf], (int)(kend - k0), ty, tx, p.beta);
         }
         buf ^= 1;
+    }
+
+    if (p.ws != nullptr) {
+        // split-K partial, folded (in split order) by conv_splitk_fold_kernel
+        float *W = p.ws + ((split * gridDim.z + img) * p.M) * p.N;
+#pragma unroll
+        for (int i = 0; i < TM; i++) {
+            const int64_t co = m0 + row_of<TM>(ty, i);
+            if (co >= p.M) continue;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int64_t pq = n0 + h * 64 + tx * 4;
+                if (pq + 3 < p.N && (p.N & 3) == 0) {
+                    *reinterpret_cast<float4 *>(W + co * p.N + pq) =
+                        make_float4(mk.get(i, h * 4), mk.get(i, h * 4 + 1), mk.get(i, h * 4 + 2), mk.get(i, h * 4 + 3));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (pq + q < p.N) W[co * p.N + pq + q] = mk.get(i, h * 4 + q);
+                }
+            }
+        }
+        return;
     }
 
 #pragma unroll
@@ -711,6 +741,21 @@ __global__ void __launch_bounds__(kThreads, 2) conv_igemm_kernel(const ConvArgs 
             if (p.epi.n) x = apply_epilogue(p.epi, x, img, co, ho, wo);
             p.o[img * p.so0 + co * p.so1 + ho * p.so2 + wo * p.so3] = x;
         }
+    }
+}
+
+// fold the conv split-K partials (split order, deterministic) + epilogue
+template <int kUnused = 0>
+__global__ void conv_splitk_fold_kernel(const ConvArgs p, int64_t n_img) {
+    const int64_t total = n_img * p.M * p.N;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        float x = p.ws[e];
+        for (int s = 1; s < p.splits; s++) x += p.ws[s * total + e];
+        const int64_t pix = e % p.N, co = (e / p.N) % p.M, img = e / (p.N * p.M);
+        const int64_t ho = pix / p.WO, wo = pix % p.WO;
+        if (p.epi.n) x = apply_epilogue(p.epi, x, img, co, ho, wo);
+        p.o[img * p.so0 + co * p.so1 + ho * p.so2 + wo * p.so3] = x;
     }
 }
 
