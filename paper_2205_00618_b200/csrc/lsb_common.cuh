@@ -106,4 +106,46 @@ __device__ __forceinline__ float apply_epilogue(const EpiStages &e, float x, int
     return x;
 }
 
+// four consecutive points along coordinate 2 (a GEMM row segment n..n+3):
+// per-stage row offsets are formed once and unit-stride operands (bias[n],
+// C_in rows) are read as one 128-bit load
+__device__ __forceinline__ float4 ldg4(const float *base, int64_t idx, int64_t stride) {
+    const float *p = base + idx;
+    if (stride == 1 && (reinterpret_cast<uintptr_t>(p) & 15) == 0) return __ldg(reinterpret_cast<const float4 *>(p));
+    if (stride == 0) {
+        const float v = __ldg(p);
+        return make_float4(v, v, v, v);
+    }
+    return make_float4(__ldg(p), __ldg(p + stride), __ldg(p + 2 * stride), __ldg(p + 3 * stride));
+}
+
+__device__ __forceinline__ void apply_epilogue4(const EpiStages &e, float (&x)[4], int64_t c0, int64_t c1,
+                                                int64_t c2, int64_t c3) {
+#pragma unroll
+    for (int i = 0; i < LSB_MAX_EPI; i++) {
+        if (i >= e.n) break;
+        const lsb_epi_stage &st = e.s[i];
+        float t[4] = {x[0], x[1], x[2], x[3]};
+        if (st.combine >= 0) {
+            const float4 v = ldg4(st.operand, c0 * st.so[0] + c1 * st.so[1] + c2 * st.so[2] + c3 * st.so[3], st.so[2]);
+            t[0] = op_rt(st.combine, t[0], v.x);
+            t[1] = op_rt(st.combine, t[1], v.y);
+            t[2] = op_rt(st.combine, t[2], v.z);
+            t[3] = op_rt(st.combine, t[3], v.w);
+        }
+        if (st.beta != 1.0f) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) t[q] = __fmul_rn(st.beta, t[q]);
+        }
+        if (st.alpha != 0.0f) {
+            const float4 c = ldg4(st.c_in, c0 * st.sc[0] + c1 * st.sc[1] + c2 * st.sc[2] + c3 * st.sc[3], st.sc[2]);
+            const float cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int q = 0; q < 4; q++) t[q] = op_rt(st.reduce, __fmul_rn(st.alpha, ew_rt(st.pre, cv[q])), t[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) x[q] = ew_rt(st.post, t[q]);
+    }
+}
+
 }  // namespace lsb

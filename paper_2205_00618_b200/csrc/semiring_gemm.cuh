@@ -619,9 +619,14 @@ __global__ void __launch_bounds__(kThreads, 2) semiring_gemm_kernel(const GemmAr
         const int64_t nq = n0 + h * 64 + tx * 4;
         float v[4];
 #pragma unroll
-        for (int q = 0; q < 4; q++)
-            v[q] = apply_epilogue(p.epi, stage[(i * 8 + h * 4 + q) * kThreads + threadIdx.x], bz, m,
-                                  nq + q, 0);
+        for (int q = 0; q < 4; q++) v[q] = stage[(i * 8 + h * 4 + q) * kThreads + threadIdx.x];
+        if (nq + 3 < p.N) {
+            apply_epilogue4(p.epi, v, bz, m, nq, 0);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (nq + q < p.N) v[q] = apply_epilogue(p.epi, v[q], bz, m, nq + q, 0);
+        }
         if (p.c_vec && nq + 3 < p.N) {
             *reinterpret_cast<float4 *>(C + m * p.sc_m + nq) = make_float4(v[0], v[1], v[2], v[3]);
         } else {

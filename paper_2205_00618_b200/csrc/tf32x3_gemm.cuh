@@ -464,8 +464,13 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                     continue;
                 }
                 if (p.epi.n) {
+                    if (n + 3 < p.N) {
+                        apply_epilogue4(p.epi, x, 0, m, n, 0);
+                    } else {
 #pragma unroll
-                    for (int e = 0; e < 4; e++) x[e] = apply_epilogue(p.epi, x[e], 0, m, n + e, 0);
+                        for (int e = 0; e < 4; e++)
+                            if (n + e < p.N) x[e] = apply_epilogue(p.epi, x[e], 0, m, n + e, 0);
+                    }
                 }
                 float *dst = p.C + m * p.sc_m;
                 if (p.c_vec && n + 3 < p.N) {
