@@ -15,8 +15,10 @@ value      device time (CUDA events on the launching stream, max over ranks),
 e2e        the same contraction through the public drop-in API
            (backend.execute) from pinned host buffers: H2D of the inputs, the
            kernels and D2H of the result inside the timed region.
-roofline   dominant kernel's achieved TFLOP/s (algorithmic 2*M*N*K / its
-           average launch duration) against the FP32 SIMT peak
+roofline   dominant kernel's achieved TFLOP/s (algorithmic 2*M*N*K / its own
+           average launch duration, CUDA events placed by liblsb around that
+           launch).  3xTF32 tensor-core path: against measured bf16 sustained
+           / 2 (tf32) / 3 (passes); SIMT path: against the FP32 peak
            148 SMs x 128 lanes x 2 flop x 1965 MHz = 74.4 TFLOP/s (computed
            from MEASURED_PEAKS.json sm_max_mhz; no measured FP32 peak exists).
 cpu_baseline  oracle/vmport.c (C restatement of the reference VM arithmetic,
