@@ -6,10 +6,12 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "lsb_dispatch.cuh"
+#include "tf32x3_conv.cuh"
 #include "tf32x3_gemm.cuh"
 
 namespace lsb {
@@ -219,6 +221,84 @@ int tf32x3_conv(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launc
     a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
     a.epi = c.epi;
     return run_main_cfg(0, ahi, alo, bhi, blo, M, P, Kp, a, s, err, errlen);
+}
+
+// the gather zero-fills out-of-range taps and indexes X with 32-bit offsets
+bool tf32x3_conv_direct_ok(const ConvArgs &c, int64_t n_img) {
+    if ((c.K + 31) / 32 * 32 > tc::CV_MAX_K || c.fill != 0.0f) return false;
+    const int64_t span = (n_img - 1) * std::llabs(c.sx0) + (c.C - 1) * std::llabs(c.sx1) +
+                         (c.H - 1) * std::llabs(c.sx2) + (c.W - 1) * std::llabs(c.sx3);
+    if (span >= ((int64_t)1 << 31) || c.sx0 < 0 || c.sx1 < 0 || c.sx2 < 0 || c.sx3 < 0) return false;
+    return load_encode();
+}
+
+// in-kernel im2col (tf32x3_conv.cuh): only the filters are pre-split
+int tf32x3_conv_direct(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err,
+                       size_t errlen) {
+    if (!tf32x3_conv_direct_ok(c, n_img)) {
+        snprintf(err, errlen, "direct tf32x3 conv needs C*R*S <= %d, a 0 fill and a < 2^31-element input",
+                 tc::CV_MAX_K);
+        return LSB_ERR_UNSUPPORTED;
+    }
+    const int64_t CO = c.M, K = c.K, P = n_img * c.N;
+    const int64_t Kp = (K + 31) / 32 * 32;
+    const size_t need = sizeof(float) * (size_t)(2 * CO) * (size_t)Kp;
+    float *ws;
+    {
+        std::lock_guard<std::mutex> lk(g_tc_mu);
+        if (need > g_split_bytes) {
+            if (g_split) {
+                cudaDeviceSynchronize();
+                cudaFree(g_split);
+                g_split = nullptr;
+                g_split_bytes = 0;
+            }
+            if (cudaMalloc(&g_split, need) != cudaSuccess) {
+                snprintf(err, errlen, "cudaMalloc(%zu) for the tf32 filters failed", need);
+                return LSB_ERR_NOMEM;
+            }
+            g_split_bytes = need;
+        }
+        g_bkey = BKey{};
+        ws = g_split;
+    }
+    float *whi = ws, *wlo = whi + CO * Kp;
+    const int64_t wtot = CO * Kp;
+    tc::filter_split_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
+        c.w, CO, K, Kp, c.R, c.S, c.sw0, c.sw1, c.sw2, c.sw3, whi, wlo);
+    if (aux_launches) *aux_launches = 1;
+    CUtensorMap mwh, mwl;
+    if (!make_map(&mwh, whi, CO, Kp, tc::CV_BK, tc::CV_BN) || !make_map(&mwl, wlo, CO, Kp, tc::CV_BK, tc::CV_BN)) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
+        return LSB_ERR_CUDA;
+    }
+    const bool row4 = c.WO % 4 == 0 && c.stride_w == 1 && c.sx3 == 1 && (c.S - 1) * c.dil_w + 3 <= 31;
+    auto kern = row4 ? tc::tf32x3_conv_kernel<true> : tc::tf32x3_conv_kernel<false>;
+    static bool attr[2] = {false, false};
+    if (!attr[row4]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::cv_smem_bytes(tc::CV_MAX_K));
+        attr[row4] = true;
+    }
+    tc::ConvTcArgs a;
+    memset(&a, 0, sizeof(a));
+    tc::ConvGeom &g = a.g;
+    g.C = c.C; g.H = c.H; g.W = c.W; g.R = c.R; g.S = c.S; g.HO = c.HO; g.WO = c.WO;
+    g.P = P; g.K = K; g.Kp = Kp;
+    g.sh = c.stride_h; g.sw = c.stride_w; g.ph = c.pad_h; g.pw = c.pad_w; g.dh = c.dil_h; g.dw = c.dil_w;
+    g.sx0 = c.sx0; g.sx1 = c.sx1; g.sx2 = c.sx2; g.sx3 = c.sx3;
+    g.fill = c.fill;
+    g.x = c.x;
+    a.CO = CO;
+    a.o = c.o;
+    a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
+    const int num_kb = (int)(Kp / tc::CV_BK);
+    a.stages_per_chunk = (num_kb + tc::CV_CHUNKS - 1) / tc::CV_CHUNKS;
+    a.epi = c.epi;
+    dim3 grid((unsigned)((P + tc::CV_BM - 1) / tc::CV_BM), (unsigned)((CO + tc::CV_BN - 1) / tc::CV_BN));
+    prof_mark(0, s);
+    kern<<<grid, tc::CV_THREADS, tc::cv_smem_bytes(Kp), s>>>(mwh, mwl, a);
+    prof_mark(1, s);
+    return LSB_OK;
 }
 
 }  // namespace lsb

@@ -470,17 +470,21 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     const bool wcontig = d->sw[3] == 1 && d->sw[2] == d->S && d->sw[1] == d->R * d->S;
     a.a_mode = (wcontig && aligned16(d->w) && d->sw[0] % 4 == 0 && K % 4 == 0) ? lsb::LD_VEC_K : lsb::LD_GENERIC;
 
-    // tensor-core path (materialised im2col + 3xTF32): opt-in only.  Measured
-    // on C3 the im2col/split prepass (8*P*K bytes) costs more than the SIMT
-    // implicit GEMM saves (0.185 ms vs 0.101 ms), so AUTO stays on SIMT.
-    bool use_tc = false;
+    // tensor cores: in-kernel im2col + 3xTF32 (tf32x3_conv.cuh) for real work
+    // and C*R*S <= 1024; the materialised-im2col variant (8*P*K bytes of
+    // prepass, slower than SIMT on C3: 0.185 vs 0.101 ms) only on request
+    int tc_mode = (2.0 * a.M * a.N * d->N * K >= (double)(1ll << 28) && a.M >= 16 &&
+                   lsb::tf32x3_conv_direct_ok(a, d->N)) ? 1 : 0;
     if (const char *env = getenv("LSB_GEMM_ALGO")) {
-        if (!strcmp(env, "tf32x3")) use_tc = lsb::tf32x3_supported(a.M, a.N * d->N, K);
+        if (!strcmp(env, "simt")) tc_mode = 0;
+        else if (!strcmp(env, "tf32x3")) tc_mode = lsb::tf32x3_conv_direct_ok(a, d->N) ? 1 : 2;
+        else if (!strcmp(env, "tf32x3_im2col")) tc_mode = 2;
     }
-    if (use_tc) {
+    if (tc_mode) {
         char err[256] = "";
         int aux = 0;
-        rc = lsb::tf32x3_conv(a, d->N, (cudaStream_t)stream, &aux, err, sizeof(err));
+        rc = tc_mode == 1 ? lsb::tf32x3_conv_direct(a, d->N, (cudaStream_t)stream, &aux, err, sizeof(err))
+                          : lsb::tf32x3_conv(a, d->N, (cudaStream_t)stream, &aux, err, sizeof(err));
         if (rc) return fail(rc, "%s", err);
         rc = check_launch("tf32x3_conv");
         if (rc) return rc;

@@ -31,6 +31,9 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
                 int64_t sb_k, int64_t sb_n, float *C, int64_t sc_m, int64_t sc_n, int c_vec, const EpiStages &epi,
                 bool b_unchanged, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
 int tf32x3_conv(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
+bool tf32x3_conv_direct_ok(const ConvArgs &c, int64_t n_img);
+int tf32x3_conv_direct(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err,
+                       size_t errlen);
 
 template <int C, int R, bool B, int BM, bool TWO = false>
 void launch_gemm(const GemmArgs &a, dim3 grid, cudaStream_t s) {

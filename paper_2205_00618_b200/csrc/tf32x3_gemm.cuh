@@ -104,6 +104,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     while (!mbar_try_wait(bar, phase)) {
     }
 }
+// blocking flavour for long waits: the thread is suspended (up to `ns`) until
+// the phase completes instead of spinning on issue slots the working warps need
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t phase, uint32_t ns = 100000) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(phase), "r"(ns)
+            : "memory");
+    }
+}
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *bar, void *dst, int x, int y) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -215,6 +229,7 @@ struct ConvGeom {
     int64_t sh, sw, ph, pw, dh, dw;
     int64_t sx0, sx1, sx2, sx3;
     float fill;
+    const float *x;   // input (used by the in-kernel im2col conv)
 };
 
 __global__ void __launch_bounds__(256) im2col_split_kernel(const float *__restrict__ x, const ConvGeom g,
@@ -291,8 +306,9 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     constexpr int kEpiWarps = Cf::kEpiWarps;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the swizzle atoms
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    // align by offsetting smem_raw itself (not through an integer) so the
+    // compiler keeps the shared address space: LDS/STS, not generic LD/ST
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * kStageBytes);
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;    // [2] chunk accumulator ready

@@ -1,0 +1,107 @@
+// Probe: tcgen05.mma kind::tf32 with an MN-major SWIZZLE_128B A operand.
+// D[128][64] = A[128][16] * B[64][16]^T, A MN-major (pixel-contiguous atoms),
+// B K-major SWIZZLE_64B; tries LBO/SBO variants and reports max error.
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include "../paper_2205_00618_b200/csrc/tf32x3_conv.cuh"
+using namespace lsb::tc;
+
+__global__ void probe(const float *A, const float *B, float *D, uint32_t lbo, uint32_t sbo, int kmajor_a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    float *sa = reinterpret_cast<float *>(smem);            // 8 KB
+    float *sb = reinterpret_cast<float *>(smem + 8192);     // 4 KB
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 12288);
+    uint32_t *slot = reinterpret_cast<uint32_t *>(smem + 12296);
+    int t = threadIdx.x;
+    for (int e = t; e < 128 * 16; e += blockDim.x) {
+        int m = e / 16, k = e % 16;
+        uint32_t off;
+        if (kmajor_a) {
+            off = (k >> 3) * 0 + m * 64 + (((k >> 2) ^ ((m >> 1) & 3)) << 4) + (k & 3) * 4;   // sw64 K-major (16 taps/row)
+        } else {
+            int r = k & 3;   // SWIZZLE_128B_BASE32B: 32-B granules XOR row (4-row atoms)
+            off = (k >> 2) * (sbo ? sbo : 2048) + (m >> 5) * (lbo ? lbo : 512) + r * 128 + ((((m & 31) >> 3) ^ r) << 5) + (m & 7) * 4;
+        }
+        sa[off / 4] = A[m * 16 + k];
+    }
+    for (int e = t; e < 64 * 16; e += blockDim.x) {
+        int n = e / 16, k = e % 16;
+        uint32_t off = n * 64 + (((k >> 2) ^ ((n >> 1) & 3)) << 4) + (k & 3) * 4;
+        sb[off / 4] = B[n * 16 + k];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (t == 0) { mbar_init(bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    if (t < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(64));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    uint32_t tmem = *slot;
+    if (t == 0) {
+        uint32_t idesc = idesc_tf32(128, 64) | (kmajor_a ? 0u : (1u << 15));
+        uint32_t abase = smem_u32(sa), bbase = smem_u32(sb);
+        for (int k = 0; k < 2; k++) {
+            uint64_t a;
+            if (kmajor_a) a = sdesc_k_sw<64>(abase) + (uint64_t)((k * 32) >> 4);
+            else {
+                a = 0;
+                a |= (uint64_t)(((abase + k * 2 * sbo) >> 4) & 0x3FFF);
+                a |= (uint64_t)(lbo >> 4) << 16;
+                a |= (uint64_t)(sbo >> 4) << 32;
+                a |= (uint64_t)1 << 46;
+                a |= (uint64_t)1 << 61;
+            }
+            uint64_t b = sdesc_k_sw<64>(bbase) + (uint64_t)((k * 32) >> 4);
+            umma_tf32(tmem, a, b, idesc, k ? 1u : 0u);
+        }
+        umma_commit(bar);
+    }
+    mbar_wait(bar, 0);
+    tc_fence_after();
+    if (t < 128) {
+        int q = (t >> 5);
+        float v[16];
+        for (int part = 0; part < 4; part++) {
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + part * 16, v);
+            for (int i = 0; i < 16; i++) D[t * 64 + part * 16 + i] = v[i];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
+}
+
+int main() {
+    float hA[128 * 16], hB[64 * 16], hD[128 * 64], ref[128 * 64];
+    srand(1);
+    for (auto &x : hA) x = (float)(rand() % 7 - 3);
+    for (auto &x : hB) x = (float)(rand() % 5 - 2);
+    for (int m = 0; m < 128; m++)
+        for (int n = 0; n < 64; n++) {
+            float s = 0;
+            for (int k = 0; k < 16; k++) s += hA[m * 16 + k] * hB[n * 16 + k];
+            ref[m * 64 + n] = s;
+        }
+    float *A, *B, *D;
+    cudaMalloc(&A, sizeof hA); cudaMalloc(&B, sizeof hB); cudaMalloc(&D, sizeof hD);
+    cudaMemcpy(A, hA, sizeof hA, cudaMemcpyHostToDevice);
+    cudaMemcpy(B, hB, sizeof hB, cudaMemcpyHostToDevice);
+    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384);
+    struct { uint32_t lbo, sbo; int km; } v[] = {{0, 0, 1}, {512, 2048, 0}, {2048, 512, 0}};
+    for (auto &c : v) {
+        cudaMemset(D, 0, sizeof hD);
+        probe<<<1, 128, 16384>>>(A, B, D, c.lbo, c.sbo, c.km);
+        cudaError_t e = cudaDeviceSynchronize();
+        cudaMemcpy(hD, D, sizeof hD, cudaMemcpyDeviceToHost);
+        double err = 0; int bad = 0;
+        for (int i = 0; i < 128 * 64; i++) { double d = fabs(hD[i] - ref[i]); if (d > err) err = d; bad += d > 1e-3; }
+        printf("kmajor=%d lbo=%u sbo=%u err=%s maxerr=%g bad=%d D[0..3]=%g %g %g %g ref=%g %g %g %g\n", c.km, c.lbo, c.sbo,
+               cudaGetErrorString(e), err, bad, hD[0], hD[1], hD[64], hD[65], ref[0], ref[1], ref[64], ref[65]);
+        if (e != cudaSuccess) return 1;
+    }
+    return 0;
+}
