@@ -12,6 +12,7 @@
 
 #include "lsb_dispatch.cuh"
 #include "tf32x3_conv.cuh"
+#include "tf32x3_conv_tma.cuh"
 #include "tf32x3_gemm.cuh"
 
 namespace lsb {
@@ -43,6 +44,26 @@ bool load_encode() {
         return false;
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     return true;
+}
+
+// the shared split workspace, grown on demand (invalidates the cached B split)
+float *acquire_ws(size_t need, char *err, size_t errlen) {
+    std::lock_guard<std::mutex> lk(g_tc_mu);
+    if (need > g_split_bytes) {
+        if (g_split) {
+            cudaDeviceSynchronize();
+            cudaFree(g_split);
+            g_split = nullptr;
+            g_split_bytes = 0;
+        }
+        if (cudaMalloc(&g_split, need) != cudaSuccess) {
+            snprintf(err, errlen, "cudaMalloc(%zu) for the tf32 operands failed", need);
+            return nullptr;
+        }
+        g_split_bytes = need;
+    }
+    g_bkey = BKey{};
+    return g_split;
 }
 
 bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int bk, int box_rows) {
@@ -211,7 +232,7 @@ int tf32x3_conv(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launc
     tc::im2col_split_kernel<<<gi, 256, 0, s>>>(c.x, g, bhi, blo);
     const int64_t wtot = M * Kp;
     tc::filter_split_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
-        c.w, M, K, Kp, c.R, c.S, c.sw0, c.sw1, c.sw2, c.sw3, ahi, alo);
+        c.w, M, K, Kp, c.C, c.R, c.S, c.sw0, c.sw1, c.sw2, c.sw3, 0, ahi, alo);
     if (aux_launches) *aux_launches = 2;
     tc::TcArgs a;
     memset(&a, 0, sizeof(a));
@@ -265,7 +286,7 @@ int tf32x3_conv_direct(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *au
     float *whi = ws, *wlo = whi + CO * Kp;
     const int64_t wtot = CO * Kp;
     tc::filter_split_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
-        c.w, CO, K, Kp, c.R, c.S, c.sw0, c.sw1, c.sw2, c.sw3, whi, wlo);
+        c.w, CO, K, Kp, c.C, c.R, c.S, c.sw0, c.sw1, c.sw2, c.sw3, 0, whi, wlo);
     if (aux_launches) *aux_launches = 1;
     CUtensorMap mwh, mwl;
     if (!make_map(&mwh, whi, CO, Kp, tc::CV_BK, tc::CV_BN) || !make_map(&mwl, wlo, CO, Kp, tc::CV_BK, tc::CV_BN)) {
@@ -295,9 +316,123 @@ int tf32x3_conv_direct(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *au
     a.stages_per_chunk = (num_kb + tc::CV_CHUNKS - 1) / tc::CV_CHUNKS;
     a.epi = c.epi;
     dim3 grid((unsigned)((P + tc::CV_BM - 1) / tc::CV_BM), (unsigned)((CO + tc::CV_BN - 1) / tc::CV_BN));
+    static long long *trace = nullptr;
+    const bool tracing = getenv("LSB_CONV_TRACE") != nullptr;
+    if (tracing) {
+        if (!trace) cudaMalloc(&trace, 11 * 64 * sizeof(long long));
+        cudaMemsetAsync(trace, 0, 11 * 64 * sizeof(long long), s);
+        a.trace = trace;
+    }
     prof_mark(0, s);
     kern<<<grid, tc::CV_THREADS, tc::cv_smem_bytes(Kp), s>>>(mwh, mwl, a);
     prof_mark(1, s);
+    if (tracing) {
+        long long h[11 * 64];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
+        FILE *f = fopen(getenv("LSB_CONV_TRACE"), "w");
+        if (f) {
+            for (int e = 0; e < 11; e++) {
+                for (int k = 0; k < 64; k++) fprintf(f, "%lld ", h[e * 64 + k]);
+                fprintf(f, "\n");
+            }
+            fclose(f);
+        }
+    }
+    return LSB_OK;
+}
+
+}  // namespace lsb
+
+namespace lsb {
+
+// TMA-fed conv (tf32x3_conv_tma.cuh): unit column stride, 4 | C, a 0 fill,
+// TMA-legal strides (16-B multiples, 16-B aligned base), row stride <= 8
+bool tf32x3_conv_tma_ok(const ConvArgs &c, int64_t n_img) {
+    const int64_t Kp = (c.K + 15) / 16 * 16;
+    if (c.stride_w != 1 || c.sx3 != 1 || c.C % 4 != 0 || c.fill != 0.0f || Kp / 4 > tc::CT_MAX_GROUPS) return false;
+    if (c.stride_h < 1 || c.stride_h > 8 || c.dil_w < 1 || c.dil_h < 1) return false;
+    if (c.sx0 % 4 || c.sx1 % 4 || c.sx2 % 4 || c.sx0 <= 0 || c.sx1 <= 0 || c.sx2 <= 0) return false;
+    if (reinterpret_cast<uintptr_t>(c.x) % 16) return false;
+    if (c.W > (1 << 30) || c.H > (1 << 30) || n_img > (1 << 30)) return false;
+    return load_encode();
+}
+
+int tf32x3_conv_tma(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen) {
+    if (!tf32x3_conv_tma_ok(c, n_img)) {
+        snprintf(err, errlen, "TMA conv needs stride_w 1, C %% 4 == 0, a 0 fill and 16-B strides");
+        return LSB_ERR_UNSUPPORTED;
+    }
+    const int64_t CO = c.M, K = c.K;
+    const int64_t Kp = (K + 15) / 16 * 16;
+    float *ws = acquire_ws(sizeof(float) * 2 * (size_t)((CO + tc::CT_BN - 1) / tc::CT_BN * tc::CT_BN) * (size_t)Kp,
+                           err, errlen);
+    if (!ws) return LSB_ERR_NOMEM;
+    const int64_t co_tiles = (CO + tc::CT_BN - 1) / tc::CT_BN;
+    const int64_t wtot = co_tiles * Kp * tc::CT_BN;
+    tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
+        c.w, CO, K, Kp, c.C, c.S, c.sw0, c.sw1, c.sw2, c.sw3, ws);
+    if (aux_launches) *aux_launches = 1;
+    CUtensorMap mx;
+    {
+        // X as (W, C, H, N) with its own strides; box 36 x 4 x 4 rows (every
+        // stride_h-th row via the element stride), zero fill out of range
+        cuuint64_t dims[4] = {(cuuint64_t)c.W, (cuuint64_t)c.C, (cuuint64_t)c.H, (cuuint64_t)n_img};
+        cuuint64_t strides[3] = {(cuuint64_t)c.sx1 * 4, (cuuint64_t)c.sx2 * 4, (cuuint64_t)c.sx0 * 4};
+        cuuint32_t box[4] = {(cuuint32_t)tc::CT_RAW_W, 4, (cuuint32_t)(4 * c.stride_h), 1};
+        cuuint32_t estr[4] = {1, 1, (cuuint32_t)c.stride_h, 1};
+        CUresult r = g_encode(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(c.x), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            snprintf(err, errlen, "cuTensorMapEncodeTiled failed (input, %d)", (int)r);
+            return LSB_ERR_CUDA;
+        }
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tc::tf32x3_conv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc::ct_smem_bytes(tc::CT_MAX_GROUPS));
+        attr = true;
+    }
+    tc::ConvTmaArgs a;
+    memset(&a, 0, sizeof(a));
+    a.C = c.C; a.K = K; a.Kp = Kp; a.R = c.R; a.S = c.S; a.HO = c.HO; a.WO = c.WO;
+    a.ph = c.pad_h; a.pw = c.pad_w; a.dh = c.dil_h; a.dw = c.dil_w; a.sh = c.stride_h;
+    a.n_img = n_img;
+    a.tiles_h = (c.HO + 3) / 4;
+    a.tiles_w = (c.WO + 31) / 32;
+    a.CO = CO;
+    a.wimg = ws;
+    if (const char *dbg = getenv("LSB_CT_DBG")) a.dbg = atoi(dbg);
+    a.o = c.o;
+    a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
+    const int num_kb = (int)(Kp / tc::CT_BK);
+    a.stages_per_chunk = (num_kb + tc::CT_CHUNKS - 1) / tc::CT_CHUNKS;
+    a.epi = c.epi;
+    dim3 grid((unsigned)(n_img * a.tiles_h * a.tiles_w), (unsigned)((CO + tc::CT_BN - 1) / tc::CT_BN));
+    static long long *trace = nullptr;
+    const char *trace_path = getenv("LSB_CONV_TRACE");
+    if (trace_path) {
+        if (!trace) cudaMalloc(&trace, 6 * 64 * sizeof(long long));
+        cudaMemsetAsync(trace, 0, 6 * 64 * sizeof(long long), s);
+        a.trace = trace;
+    }
+    prof_mark(0, s);
+    tc::tf32x3_conv_tma_kernel<<<grid, tc::CT_THREADS, tc::ct_smem_bytes(Kp / 4), s>>>(mx, a);
+    prof_mark(1, s);
+    if (trace_path) {
+        long long h[6 * 64];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
+        if (FILE *f = fopen(trace_path, "w")) {
+            for (int e = 0; e < 6; e++) {
+                for (int k = 0; k < 64; k++) fprintf(f, "%lld ", h[e * 64 + k]);
+                fprintf(f, "\n");
+            }
+            fclose(f);
+        }
+    }
     return LSB_OK;
 }
 

@@ -50,7 +50,13 @@ struct ConvTcArgs {
     int64_t so[4];        // n, co, h, w
     int stages_per_chunk;
     EpiStages epi;
+    long long *trace;     // debug: per-stage clock64 stamps of CTA 0 (null = off)
 };
+
+#define CV_TRACE(ev, kb)                                                              \
+    do {                                                                              \
+        if (p.trace != nullptr && blockIdx.x == 0 && (kb) < 64) p.trace[(ev) * 64 + (kb)] = clock64(); \
+    } while (0)
 
 // MN-major tf32 operand in the SWIZZLE_128B_BASE32B canonical layout (the
 // only MN-major layout the tensor core takes for 32-bit types): atoms of
@@ -80,6 +86,21 @@ __device__ __forceinline__ float split_hi(float x) {
 }
 __device__ __forceinline__ float split_lo(float x, float hi) {
     return fabsf(hi) == __int_as_float(0x7f800000) ? 0.0f : x - hi;
+}
+
+// predicated read-only load, 0 when !ok (plain PTX predication: the C++
+// ternary on __ldg made ptxas rebuild the memory descriptor per load)
+__device__ __forceinline__ float ldg_or_zero(const float *p, uint32_t ok) {
+    float v;
+    // volatile: keeps the load where the software pipeline issues it (a
+    // plain asm/__ldg gets sunk next to its first use under register pressure)
+    asm volatile("{\n\t.reg .pred q;\n\t"
+        "setp.ne.u32 q, %2, 0;\n\t"
+        "mov.f32 %0, 0f00000000;\n\t"
+        "@q ld.global.nc.f32 %0, [%1];\n\t}"
+        : "=f"(v)
+        : "l"(p), "r"(ok));
+    return v;
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -163,6 +184,7 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
             uint32_t phase = 0;
             for (int kb = 0; kb < num_kb; kb++) {
                 mbar_wait_sleep(&empty[stage], phase ^ 1);
+                CV_TRACE(0, kb);
                 unsigned char *base = smem + stage * CV_STAGE_BYTES;
                 mbar_expect_tx(&full[stage], 2 * CV_TILE_B);
                 tma_load_2d(&map_whi, &full[stage], base + 2 * CV_TILE_A, kb * CV_BK, (int)c0);
@@ -181,6 +203,7 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
             uint32_t phase = 0;
             for (int kb = 0; kb < num_kb; kb++) {
                 mbar_wait_sleep(&full[stage], phase);
+                CV_TRACE(1, kb);
                 tc_fence_after();
                 const int chunk = kb / p.stages_per_chunk;
                 const uint32_t d = tmem + (uint32_t)(chunk * CV_BN);
@@ -244,6 +267,7 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
         const uint32_t off0 = chunk_off(2 * cw), off1 = chunk_off(2 * cw + 1);
 
         auto load = [&](int kb, float (&v)[8]) {
+            if (lane == 0 && (cw == 0 || cw == 7)) CV_TRACE(2 + (cw ? 4 : 0), kb);
 #pragma unroll
             for (int t2 = 0; t2 < 2; t2++) {
                 const int4 t = taps[kb * CV_BK + 2 * cw + t2];
@@ -251,12 +275,12 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
                     const uint32_t m = ((unsigned)(hb[0] + t.y) < H) ? (wmask >> t.z) : 0u;
                     const float *src = x + (pb[0] + t.x);
 #pragma unroll
-                    for (int i = 0; i < 4; i++) v[t2 * 4 + i] = (m >> i) & 1u ? __ldg(src + i) : 0.0f;
+                    for (int i = 0; i < 4; i++) v[t2 * 4 + i] = ldg_or_zero(src + i, (m >> i) & 1u);
                 } else {
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
                         const bool ok = ((unsigned)(hb[i] + t.y) < H) & ((unsigned)(wb[i] + t.z) < W);
-                        v[t2 * 4 + i] = ok ? __ldg(x + (pb[i] + t.x)) : 0.0f;
+                        v[t2 * 4 + i] = ldg_or_zero(x + (pb[i] + t.x), ok);
                     }
                 }
             }
@@ -269,7 +293,9 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
                 h[i] = split_hi(v[i]);
                 l[i] = split_lo(v[i], h[i]);
             }
+            if (lane == 0 && (cw == 0 || cw == 7)) CV_TRACE(3 + (cw ? 4 : 0), kb);
             mbar_wait_sleep(&empty[slot], (uint32_t)(((kb / CV_STAGES) & 1) ^ 1));
+            if (lane == 0 && (cw == 0 || cw == 7)) CV_TRACE(4 + (cw ? 4 : 0), kb);
             const uint32_t sb = sbase + (uint32_t)(slot * CV_STAGE_BYTES);
             asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sb + off0), "f"(h[0]), "f"(h[1]),
                          "f"(h[2]), "f"(h[3]) : "memory");
@@ -282,22 +308,29 @@ __global__ void __launch_bounds__(CV_THREADS, 2)
             fence_proxy_async_smem();   // generic-proxy stores -> visible to the tensor core
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[slot]);
+            if (lane == 0 && (cw == 0 || cw == 7)) CV_TRACE(5 + (cw ? 4 : 0), kb);
         };
-        // software pipeline: the loads of stage kb+1 are in flight while
-        // stage kb is split and stored
-        float va[8], vb[8];
+        // software pipeline: the loads of stages kb+1 and kb+2 are in flight
+        // while stage kb is split and stored
+        float va[8], vb[8], vc[8];
         load(0, va);
-        for (int kb = 0; kb < num_kb; kb += 2) {
-            if (kb + 1 < num_kb) load(kb + 1, vb);
+        if (num_kb > 1) load(1, vb);
+        for (int kb = 0; kb < num_kb; kb += 3) {
+            if (kb + 2 < num_kb) load(kb + 2, vc);
             store(kb, va);
             if (kb + 1 < num_kb) {
-                if (kb + 2 < num_kb) load(kb + 2, va);
+                if (kb + 3 < num_kb) load(kb + 3, va);
                 store(kb + 1, vb);
+            }
+            if (kb + 2 < num_kb) {
+                if (kb + 4 < num_kb) load(kb + 4, vb);
+                store(kb + 2, vc);
             }
         }
 
         // ---------------- epilogue: TMEM (4 chunk accumulators) -> fp32 sum
         mbar_wait_sleep(tdone, 0);
+        if (lane == 0 && cw == 0) CV_TRACE(10, 0);
         tc_fence_after();
         float *tile = reinterpret_cast<float *>(smem);   // [CV_BN][CV_BM], all stages retired
         if (warp < 6) {

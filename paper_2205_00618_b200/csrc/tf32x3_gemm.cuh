@@ -274,17 +274,31 @@ __global__ void __launch_bounds__(256) im2col_split_kernel(const float *__restri
 }
 
 // Conv prepass: filters w[co, c, r, s] (any strides) -> hi/lo [CO][Kp]
+// filters W[co][c][r][s] -> hi/lo [co][Kp]; tap order k = (c, r, s) or, with
+// rsc, k = (r, s, c) (the TMA conv's 4-channel groups)
 __global__ void __launch_bounds__(256) filter_split_kernel(const float *__restrict__ w, int64_t CO, int64_t K,
-                                                           int64_t Kp, int64_t R, int64_t S, int64_t sw0,
-                                                           int64_t sw1, int64_t sw2, int64_t sw3,
-                                                           float *__restrict__ hi, float *__restrict__ lo) {
+                                                           int64_t Kp, int64_t C, int64_t R, int64_t S,
+                                                           int64_t sw0, int64_t sw1, int64_t sw2, int64_t sw3,
+                                                           int rsc, float *__restrict__ hi,
+                                                           float *__restrict__ lo) {
     const int64_t total = CO * Kp;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t co = e / Kp, k = e % Kp;
         float v = 0.0f;
         if (k < K) {
-            const int64_t rs = R * S, c = k / rs, r = (k % rs) / S, s = k % S;
+            int64_t c, r, s;
+            if (rsc) {
+                const int64_t rs = k / C;
+                c = k % C;
+                r = rs / S;
+                s = rs % S;
+            } else {
+                const int64_t rs = R * S;
+                c = k / rs;
+                r = (k % rs) / S;
+                s = k % S;
+            }
             v = __ldg(w + co * sw0 + c * sw1 + r * sw2 + s * sw3);
         }
         const float h = rna_tf32(v);

@@ -1,4 +1,5 @@
-"""Run the C3 conv through the C ABI repeatedly (ncu target)."""
+"""Time the C3 conv through the C ABI: eager (host overhead included) and
+CUDA-graph replay (device time), plus LSB profile of the conv kernel alone."""
 import os
 import sys
 import numpy as np
@@ -24,4 +25,24 @@ for _ in range(20):
     backend.run_device(k, ptrs, s)
 e1.record()
 torch.cuda.synchronize()
-print("conv ms", e0.elapsed_time(e1) / 20)
+print("conv ms (eager, host-bound)", e0.elapsed_time(e1) / 20)
+if reps > 1 and not os.environ.get("LSB_CONV_TRACE"):
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(20):
+                backend.run_device(k, ptrs, side.cuda_stream)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    print("conv ms (graph)", e0.elapsed_time(e1) / 20)
+    native.profile(True)
+    backend.run_device(k, ptrs, s)
+    torch.cuda.synchronize()
+    print("conv kernel ms (profile)", native.last_kernel_ms())
+    native.profile(False)

@@ -75,7 +75,65 @@ __global__ void probe(const float *A, const float *B, float *D, uint32_t lbo, ui
     if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
 }
 
+__global__ void mma_lat(int kmajor_a, int n_iter, int per, long long *out, int nn) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 32768);
+    uint32_t *slot = reinterpret_cast<uint32_t *>(smem + 32776);
+    int t = threadIdx.x;
+    for (int e = t; e < 8192; e += blockDim.x) reinterpret_cast<float *>(smem)[e] = 0.5f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (t == 0) { mbar_init(bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    if (t < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    uint32_t tmem = *slot;
+    if (t == 0) {
+        uint32_t idesc = idesc_tf32(128, nn) | (kmajor_a ? 0u : (1u << 15));
+        uint32_t base = smem_u32(smem);
+        uint64_t a = kmajor_a ? sdesc_k_sw<64>(base) : sdesc_mn_sw128_32b(base);
+        uint64_t b = sdesc_k_sw<64>(base + 16384);
+        long long t0 = clock64();
+        for (int it = 0; it < n_iter; it++) {
+            for (int j = 0; j < per; j++) umma_tf32(tmem, a, b, idesc, 1u);
+            umma_commit(bar);
+            mbar_wait(bar, it & 1);
+        }
+        long long t1 = clock64();
+        out[0] = t1 - t0;
+        // throughput: no waits
+        t0 = clock64();
+        for (int it = 0; it < n_iter; it++)
+            for (int j = 0; j < per; j++) umma_tf32(tmem, a, b, idesc, 1u);
+        umma_commit(bar);
+        mbar_wait(bar, n_iter & 1);
+        t1 = clock64();
+        out[1] = t1 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
 int main() {
+    {
+        long long *o, h[2];
+        cudaMalloc(&o, 16);
+        cudaFuncSetAttribute(mma_lat, cudaFuncAttributeMaxDynamicSharedMemorySize, 40000);
+        for (int km = 0; km < 2; km++)
+            for (int nn : {64, 128, 256})
+            for (int per : {6}) {
+                mma_lat<<<1, 128, 40000>>>(km, 200, per, o, nn);
+                cudaError_t e = cudaDeviceSynchronize();
+                cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
+                printf("kmajor=%d N=%d per=%d %s: latency/iter %.1f cyc, throughput %.1f cyc/mma\n", km, nn, per,
+                       cudaGetErrorString(e), h[0] / 200.0, h[1] / (200.0 * per));
+            }
+    }
     float hA[128 * 16], hB[64 * 16], hD[128 * 64], ref[128 * 64];
     srand(1);
     for (auto &x : hA) x = (float)(rand() % 7 - 3);
