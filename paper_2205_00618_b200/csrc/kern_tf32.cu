@@ -13,6 +13,7 @@
 #include "lsb_dispatch.cuh"
 #include "tf32x3_conv.cuh"
 #include "tf32x3_conv_tma.cuh"
+#include "tf32x3_conv_nhwc.cuh"
 #include "tf32x3_gemm.cuh"
 
 namespace lsb {
@@ -371,7 +372,7 @@ int tf32x3_conv_tma(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_l
     const int64_t co_tiles = (CO + tc::CT_BN - 1) / tc::CT_BN;
     const int64_t wtot = co_tiles * Kp * tc::CT_BN;
     tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
-        c.w, CO, K, Kp, c.C, c.S, c.sw0, c.sw1, c.sw2, c.sw3, ws);
+        c.w, CO, K, Kp, c.C, c.C, c.S, c.sw0, c.sw1, c.sw2, c.sw3, ws);
     if (aux_launches) *aux_launches = 1;
     CUtensorMap mx;
     {
@@ -427,6 +428,104 @@ int tf32x3_conv_tma(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_l
         cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
         if (FILE *f = fopen(trace_path, "w")) {
             for (int e = 0; e < 6; e++) {
+                for (int k = 0; k < 64; k++) fprintf(f, "%lld ", h[e * 64 + k]);
+                fprintf(f, "\n");
+            }
+            fclose(f);
+        }
+    }
+    return LSB_OK;
+}
+
+}  // namespace lsb
+
+namespace lsb {
+
+// NHWC-copy conv (tf32x3_conv_nhwc.cuh): zero fill, any input strides (the
+// prepass absorbs them), row/column strides <= 8 (TMA element strides)
+bool tf32x3_conv_nhwc_ok(const ConvArgs &c, int64_t n_img) {
+    if (c.fill != 0.0f || c.stride_h < 1 || c.stride_h > 8 || c.stride_w < 1 || c.stride_w > 8) return false;
+    if (c.dil_h < 1 || c.dil_w < 1 || c.W > (1 << 30) || n_img * c.H > 65535) return false;   // prepass grid.z
+    const int64_t Cp = (c.C + 15) / 16 * 16;
+    if (c.R * c.S * Cp / tc::CN_BK < 1) return false;
+    return load_encode();
+}
+
+int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err,
+                     size_t errlen) {
+    if (!tf32x3_conv_nhwc_ok(c, n_img)) {
+        snprintf(err, errlen, "NHWC tensor-core conv needs a 0 fill and strides <= 8");
+        return LSB_ERR_UNSUPPORTED;
+    }
+    const int64_t CO = c.M, Cp = (c.C + 15) / 16 * 16, K = c.R * c.S * Cp;
+    const int64_t co_tiles = (CO + tc::CN_BN - 1) / tc::CN_BN;
+    const size_t xel = (size_t)n_img * c.H * c.W * Cp;
+    const size_t wel = 2 * (size_t)co_tiles * tc::CN_BN * (size_t)K;
+    float *ws = acquire_ws(sizeof(float) * (2 * xel + wel), err, errlen);
+    if (!ws) return LSB_ERR_NOMEM;
+    float *xhi = ws, *xlo = xhi + xel, *wimg = xlo + xel;
+    {
+        dim3 g((unsigned)((c.W + 31) / 32), (unsigned)((Cp + 31) / 32), (unsigned)(n_img * c.H));
+        tc::nchw_split_nhwc_kernel<<<g, 256, 0, s>>>(c.x, c.C, c.H, c.W, Cp, c.sx0, c.sx1, c.sx2, c.sx3, xhi, xlo);
+        const int64_t wtot = co_tiles * tc::CN_BN * K;
+        tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
+            c.w, CO, K, K, c.C, Cp, c.S, c.sw0, c.sw1, c.sw2, c.sw3, wimg);
+        if (aux_launches) *aux_launches = 2;
+    }
+    CUtensorMap mh, ml;
+    {
+        cuuint64_t dims[4] = {(cuuint64_t)Cp, (cuuint64_t)c.W, (cuuint64_t)c.H, (cuuint64_t)n_img};
+        cuuint64_t strides[3] = {(cuuint64_t)Cp * 4, (cuuint64_t)(c.W * Cp) * 4, (cuuint64_t)(c.H * c.W * Cp) * 4};
+        cuuint32_t box[4] = {(cuuint32_t)tc::CN_BK, (cuuint32_t)(32 * c.stride_w), (cuuint32_t)(4 * c.stride_h), 1};
+        cuuint32_t estr[4] = {1, (cuuint32_t)c.stride_w, (cuuint32_t)c.stride_h, 1};
+        for (int i = 0; i < 2; i++) {
+            CUresult r = g_encode(i ? &ml : &mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, i ? xlo : xhi, dims, strides, box,
+                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                snprintf(err, errlen, "cuTensorMapEncodeTiled failed (NHWC input, %d)", (int)r);
+                return LSB_ERR_CUDA;
+            }
+        }
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tc::tf32x3_conv_nhwc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc::CN_SMEM);
+        attr = true;
+    }
+    tc::ConvNhwcArgs a;
+    memset(&a, 0, sizeof(a));
+    a.Cp = Cp; a.R = c.R; a.S = c.S; a.HO = c.HO; a.WO = c.WO;
+    a.ph = c.pad_h; a.pw = c.pad_w; a.dh = c.dil_h; a.dw = c.dil_w; a.sh = c.stride_h; a.sw = c.stride_w;
+    a.tiles_h = (c.HO + 3) / 4;
+    a.tiles_w = (c.WO + 31) / 32;
+    a.CO = CO;
+    a.wimg = wimg;
+    a.o = c.o;
+    a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
+    const int num_kb = (int)(K / tc::CN_BK);
+    a.stages_per_chunk = (num_kb + tc::CN_CHUNKS - 1) / tc::CN_CHUNKS;
+    a.vec4 = c.WO % 4 == 0 && c.so3 == 1 && c.so2 % 4 == 0 && c.so1 % 4 == 0 && c.so0 % 4 == 0 &&
+             reinterpret_cast<uintptr_t>(c.o) % 16 == 0;
+    a.epi = c.epi;
+    dim3 grid((unsigned)(n_img * a.tiles_h * a.tiles_w), (unsigned)co_tiles);
+    static long long *trace = nullptr;
+    const char *trace_path = getenv("LSB_CONV_TRACE");
+    if (trace_path) {
+        if (!trace) cudaMalloc(&trace, 3 * 64 * sizeof(long long));
+        cudaMemsetAsync(trace, 0, 3 * 64 * sizeof(long long), s);
+        a.trace = trace;
+    }
+    prof_mark(0, s);
+    tc::tf32x3_conv_nhwc_kernel<<<grid, tc::CN_THREADS, tc::CN_SMEM, s>>>(mh, ml, a);
+    prof_mark(1, s);
+    if (trace_path) {
+        long long h[3 * 64];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
+        if (FILE *f = fopen(trace_path, "w")) {
+            for (int e = 0; e < 3; e++) {
                 for (int k = 0; k < 64; k++) fprintf(f, "%lld ", h[e * 64 + k]);
                 fprintf(f, "\n");
             }

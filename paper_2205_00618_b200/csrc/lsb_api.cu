@@ -473,14 +473,17 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     // tensor cores: in-kernel im2col + 3xTF32 (tf32x3_conv.cuh) for real work
     // and C*R*S <= 1024; the materialised-im2col variant (8*P*K bytes of
     // prepass, slower than SIMT on C3: 0.185 vs 0.101 ms) only on request
-    // tc_mode: 3 = TMA-fed (stride-1 columns, 4 | C), 1 = in-kernel gather,
-    // 2 = materialised im2col (on request only), 0 = SIMT
+    // tc_mode: 4 = NHWC hi/lo copy + pure TMA->MMA, 3 = TMA-fed raw NCHW
+    // boxes + converter warps, 1 = in-kernel gather, 2 = materialised im2col
+    // (on request only), 0 = SIMT
     const bool big = 2.0 * a.M * a.N * d->N * K >= (double)(1ll << 28) && a.M >= 16;
+    const bool nhwc_ok = lsb::tf32x3_conv_nhwc_ok(a, d->N);
     const bool tma_ok = lsb::tf32x3_conv_tma_ok(a, d->N), gather_ok = lsb::tf32x3_conv_direct_ok(a, d->N);
-    int tc_mode = big ? (tma_ok ? 3 : gather_ok ? 1 : 0) : 0;
+    int tc_mode = big ? (nhwc_ok ? 4 : tma_ok ? 3 : gather_ok ? 1 : 0) : 0;
     if (const char *env = getenv("LSB_GEMM_ALGO")) {
         if (!strcmp(env, "simt")) tc_mode = 0;
-        else if (!strcmp(env, "tf32x3")) tc_mode = tma_ok ? 3 : gather_ok ? 1 : 2;
+        else if (!strcmp(env, "tf32x3")) tc_mode = nhwc_ok ? 4 : tma_ok ? 3 : gather_ok ? 1 : 2;
+        else if (!strcmp(env, "tf32x3_tma")) tc_mode = tma_ok ? 3 : 2;
         else if (!strcmp(env, "tf32x3_gather")) tc_mode = gather_ok ? 1 : 2;
         else if (!strcmp(env, "tf32x3_im2col")) tc_mode = 2;
     }
@@ -488,7 +491,8 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
         char err[256] = "";
         int aux = 0;
         cudaStream_t st = (cudaStream_t)stream;
-        rc = tc_mode == 3   ? lsb::tf32x3_conv_tma(a, d->N, st, &aux, err, sizeof(err))
+        rc = tc_mode == 4   ? lsb::tf32x3_conv_nhwc(a, d->N, st, &aux, err, sizeof(err))
+             : tc_mode == 3 ? lsb::tf32x3_conv_tma(a, d->N, st, &aux, err, sizeof(err))
              : tc_mode == 1 ? lsb::tf32x3_conv_direct(a, d->N, st, &aux, err, sizeof(err))
                             : lsb::tf32x3_conv(a, d->N, st, &aux, err, sizeof(err));
         if (rc) return fail(rc, "%s", err);

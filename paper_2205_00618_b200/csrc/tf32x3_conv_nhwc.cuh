@@ -1,0 +1,285 @@
+// tf32x3_conv_nhwc.cuh -- NCHW direct convolution on the tensor cores through
+// an NHWC hi/lo copy of the input: implicit GEMM D[pixel][co] = Σ_(r,s,c)
+// X[pixel, tap] W[co, tap] in split-TF32 (Xhi.Whi + Xhi.Wlo + Xlo.Whi).
+//
+// Prepass (nchw_split_nhwc_kernel): X (any strides) -> Xhi, Xlo as [N][H][W][Cp]
+// (channels innermost, zero padded to Cp = 16k).  With channels innermost a
+// 16-channel x 32-column x 4-row box is exactly a K-major SWIZZLE_64B UMMA
+// operand (128 pixel rows of 64 B), and the tap's (r, s) shift lands on
+// non-innermost TMA coordinates, which may be any integer (out of range ->
+// zero fill = the conv padding; stride via TMA element strides).  So the
+// mainloop is the GEMM kernel's: no converter warps, no proxy fence, every
+// operand byte moved by TMA.
+//   warp 0      TMA: Xhi box, Xlo box, one 8 KiB bulk copy of the stage's
+//               filter image (hi | lo, tf32x3_conv_tma.cuh:filter_image_kernel)
+//   warp 1      TMEM allocator + tcgen05.mma issuer: N=128 (Xhi x [Whi|Wlo])
+//               + N=64 (Xlo x Whi) per 8 taps
+//   warps 2-9   epilogue: TMEM -> fp32 sum of the two accumulators of both
+//               K halves -> smem [co][pixel] -> NCHW stores (fused stages)
+// Tile: 4 output rows x 32 output columns of one image (M = 128), 64 channels.
+#pragma once
+
+#include "tf32x3_conv_tma.cuh"
+
+namespace lsb {
+namespace tc {
+
+constexpr int CN_BN = 64;
+constexpr int CN_BK = 16;                 // channels per stage (one (r, s) tap)
+constexpr int CN_STAGES = 4;
+constexpr int CN_EPI_WARPS = 8;
+constexpr int CN_THREADS = 64 + 32 * CN_EPI_WARPS;   // 320
+constexpr int CN_CHUNKS = 2;
+constexpr int CN_ACC_COLS = 2 * CN_BN;
+constexpr int CN_TILE_A = 128 * CN_BK * 4;           // 8 KiB
+constexpr int CN_TILE_B = 2 * CN_BN * CN_BK * 4;     // 8 KiB (hi | lo)
+constexpr int CN_STAGE = 2 * CN_TILE_A + CN_TILE_B;  // 24 KiB
+constexpr size_t CN_SMEM = (size_t)CN_STAGES * CN_STAGE + 256 + 1024;
+static_assert(CN_STAGES * CN_STAGE >= CN_BN * 128 * 4, "epilogue staging reuses the stages");
+
+struct ConvNhwcArgs {
+    int64_t Cp, R, S, HO, WO, ph, pw, dh, dw, sh, sw;
+    int64_t tiles_h, tiles_w, CO;
+    const float *wimg;
+    float *o;
+    int64_t so[4];
+    int stages_per_chunk;
+    int vec4;             // float4 output stores (see the epilogue)
+    EpiStages epi;
+    long long *trace;     // debug (LSB_CN_TRACE builds): per-stage clock64 stamps of CTA 0
+};
+
+#ifdef LSB_CN_TRACE
+#define CN_TRACE(ev, kb)                                                                          \
+    do {                                                                                          \
+        if (p.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && (kb) < 64)               \
+            p.trace[(ev) * 64 + (kb)] = clock64();                                                \
+    } while (0)
+#else
+#define CN_TRACE(ev, kb) \
+    do {                 \
+    } while (0)
+#endif
+
+// X[n][c][h][w] (element strides sx*) -> hi/lo [n][h][w][Cp], channels >= C
+// zero; 32 x 32 (w, c) tiles through smem so both sides are coalesced
+__global__ void __launch_bounds__(256) nchw_split_nhwc_kernel(const float *__restrict__ x, int64_t C, int64_t H,
+                                                              int64_t W, int64_t Cp, int64_t sx0, int64_t sx1,
+                                                              int64_t sx2, int64_t sx3, float *__restrict__ hi,
+                                                              float *__restrict__ lo) {
+    __shared__ float tile[32][33];
+    const int64_t nh = blockIdx.z;   // n * H + h
+    const int64_t n = nh / H, h = nh % H;
+    const int64_t w0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int cc = ty + 8 * j;
+        const int64_t c = c0 + cc, w = w0 + tx;
+        tile[cc][tx] = (c < C && w < W) ? __ldg(x + n * sx0 + c * sx1 + h * sx2 + w * sx3) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int ww = ty + 8 * j;
+        const int64_t w = w0 + ww, c = c0 + tx;
+        if (w < W && c < Cp) {
+            const float v = tile[tx][ww];
+            const float vh = rna_tf32(v);
+            const int64_t o = ((nh * W) + w) * Cp + c;
+            hi[o] = vh;
+            lo[o] = rna_tf32(v - vh);
+        }
+    }
+}
+
+// grid: x = image * tiles_h * tiles_w output tiles, y = channel tiles
+__global__ void __launch_bounds__(CN_THREADS, 2)
+    tf32x3_conv_nhwc_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
+                            const ConvNhwcArgs p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + CN_STAGES * CN_STAGE);
+    uint64_t *empty = full + CN_STAGES;
+    uint64_t *tdone = empty + CN_STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tdone + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int64_t t = blockIdx.x;
+    const int tw = (int)(t % p.tiles_w);
+    t /= p.tiles_w;
+    const int th = (int)(t % p.tiles_h);
+    const int n = (int)(t / p.tiles_h);
+    const int h0 = th * 4, w0 = tw * 32;
+    const int64_t c0 = (int64_t)blockIdx.y * CN_BN;
+    const int cblocks = (int)(p.Cp / CN_BK);
+    const int num_kb = (int)(p.R * p.S) * cblocks;
+    if (threadIdx.x == 0) CN_TRACE(2, 2);
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&map_hi);
+        tma_prefetch_desc(&map_lo);
+        for (int s = 0; s < CN_STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tdone, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(CN_CHUNKS * CN_ACC_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            const int hin0 = (int)(h0 * p.sh - p.ph), win0 = (int)(w0 * p.sw - p.pw);
+            int stage = 0;
+            uint32_t phase = 0;
+            int cb = 0, s = 0, r = 0;
+            for (int kb = 0; kb < num_kb; kb++) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                CN_TRACE(0, kb);
+                unsigned char *base = smem + stage * CN_STAGE;
+                mbar_expect_tx(&full[stage], CN_STAGE);
+                const int hi_ = hin0 + r * (int)p.dh, wi = win0 + s * (int)p.dw;
+                tma_load_4d(&map_hi, &full[stage], base, cb * CN_BK, wi, hi_, n);
+                tma_load_4d(&map_lo, &full[stage], base + CN_TILE_A, cb * CN_BK, wi, hi_, n);
+                bulk_load(base + 2 * CN_TILE_A, p.wimg + ((int64_t)blockIdx.y * num_kb + kb) * (2 * CN_BN * CN_BK),
+                          CN_TILE_B, &full[stage]);
+                if (++cb == cblocks) {
+                    cb = 0;
+                    if (++s == p.S) {
+                        s = 0;
+                        ++r;
+                    }
+                }
+                if (++stage == CN_STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (A and B K-major SWIZZLE_64B)
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(128, CN_BN);
+            constexpr uint32_t idesc_n128 = idesc_tf32(128, 2 * CN_BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int kb = 0; kb < num_kb; kb++) {
+                mbar_wait(&full[stage], phase);
+                CN_TRACE(1, kb);
+                tc_fence_after();
+                const int chunk = kb / p.stages_per_chunk;
+                const uint32_t d = tmem + (uint32_t)(chunk * CN_ACC_COLS);
+                const uint32_t base = smem_u32(smem + stage * CN_STAGE);
+                const uint64_t ahi = sdesc_k_sw<64>(base), alo = sdesc_k_sw<64>(base + CN_TILE_A);
+                const uint64_t bhi = sdesc_k_sw<64>(base + 2 * CN_TILE_A);
+#pragma unroll
+                for (int k = 0; k < CN_BK / 8; k++) {
+                    const uint64_t off = (uint64_t)((k * 32) >> 4);
+                    const uint32_t first = (kb % p.stages_per_chunk == 0 && k == 0) ? 0u : 1u;
+                    umma_tf32(d, ahi + off, bhi + off, idesc_n128, first);
+                    umma_tf32(d, alo + off, bhi + off, idesc, 1u);
+                }
+                umma_commit(&empty[stage]);
+                if (++stage == CN_STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            umma_commit(tdone);
+        }
+    } else {
+        // ---------------- epilogue (warps 2..9)
+        const int ew = warp - 2;
+        mbar_wait(tdone, 0);
+        if (ew == 0 && lane == 0) CN_TRACE(2, 0);
+        tc_fence_after();
+        float *tile = reinterpret_cast<float *>(smem);   // [CN_BN][128]
+        {
+            const int qd = warp & 3, half = ew >> 2;
+            const int row = qd * 32 + lane;
+            const int nch = (num_kb + p.stages_per_chunk - 1) / p.stages_per_chunk;
+#pragma unroll
+            for (int part = 0; part < 2; part++) {
+                const int col = half * 32 + part * 16;
+                uint32_t rr[CN_CHUNKS][2][16];
+#pragma unroll
+                for (int ch = 0; ch < CN_CHUNKS; ch++)
+                    if (ch < nch) {
+                        const uint32_t ta = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ch * CN_ACC_COLS + col);
+                        tmem_ld16_issue(ta, rr[ch][0]);
+                        tmem_ld16_issue(ta + CN_BN, rr[ch][1]);
+                    }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                    float acc = __uint_as_float(rr[0][0][i]) + __uint_as_float(rr[0][1][i]);
+#pragma unroll
+                    for (int ch = 1; ch < CN_CHUNKS; ch++)
+                        if (ch < nch) acc += __uint_as_float(rr[ch][0][i]) + __uint_as_float(rr[ch][1][i]);
+                    tile[(col + i) * 128 + row] = acc;
+                }
+            }
+        }
+        if (ew == 0 && lane == 0) CN_TRACE(2, 3);
+        tc_fence_before();
+        asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
+        if (ew == 0 && lane == 0) CN_TRACE(2, 4);
+        if (p.vec4) {
+            // one float4 per lane: lane -> output row h = lane / 8, columns
+            // w0 + 4 (lane % 8) .. +3; a warp stores one channel's 4 x 32 tile
+            // (WO % 4 == 0, unit column stride, 16-B aligned rows)
+            const int h = lane >> 3, w4 = (lane & 7) * 4;
+            const int ho = h0 + h, wo = w0 + w4;
+            const bool ok = ho < p.HO && wo < p.WO;
+            for (int co_l = ew; co_l < CN_BN; co_l += CN_EPI_WARPS) {
+                const int64_t co = c0 + co_l;
+                if (co >= p.CO) break;
+                float4 v = *reinterpret_cast<const float4 *>(&tile[co_l * 128 + h * 32 + w4]);
+                if (p.epi.n) {
+                    v.x = apply_epilogue(p.epi, v.x, n, co, ho, wo);
+                    v.y = apply_epilogue(p.epi, v.y, n, co, ho, wo + 1);
+                    v.z = apply_epilogue(p.epi, v.z, n, co, ho, wo + 2);
+                    v.w = apply_epilogue(p.epi, v.w, n, co, ho, wo + 3);
+                }
+                if (ok)
+                    *reinterpret_cast<float4 *>(p.o + n * p.so[0] + co * p.so[1] + (int64_t)ho * p.so[2] + wo) = v;
+            }
+        } else {
+            const int wo = w0 + lane;
+            for (int co_l = ew; co_l < CN_BN; co_l += CN_EPI_WARPS) {
+                const int64_t co = c0 + co_l;
+                if (co >= p.CO) break;
+                float *orow = p.o + n * p.so[0] + co * p.so[1] + wo * p.so[3];
+#pragma unroll
+                for (int h = 0; h < 4; h++) {
+                    const int ho = h0 + h;
+                    if (ho >= p.HO || wo >= p.WO) continue;
+                    float v = tile[co_l * 128 + h * 32 + lane];
+                    if (p.epi.n) v = apply_epilogue(p.epi, v, n, co, ho, wo);
+                    orow[(int64_t)ho * p.so[2]] = v;
+                }
+            }
+        }
+        if (ew == 0 && lane == 0) CN_TRACE(2, 5);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) CN_TRACE(2, 1);
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CN_CHUNKS * CN_ACC_COLS));
+    }
+}
+
+}  // namespace tc
+}  // namespace lsb

@@ -106,9 +106,10 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 // operand: [co tile][stage][hi | lo][64 co rows x 16 taps, K-major SWIZZLE_64B],
 // taps in (r, s, c) order, so one 8 KiB bulk copy feeds a stage (a 2-D TMA
 // box of 64-B rows costs one request per row)
+// (tap k -> (r, s) = k / Cp, channel c = k % Cp; zero for c >= C or k >= K)
 __global__ void __launch_bounds__(256) filter_image_kernel(const float *__restrict__ w, int64_t CO, int64_t K,
-                                                           int64_t Kp, int64_t C, int64_t S, int64_t sw0,
-                                                           int64_t sw1, int64_t sw2, int64_t sw3,
+                                                           int64_t Kp, int64_t C, int64_t Cp, int64_t S,
+                                                           int64_t sw0, int64_t sw1, int64_t sw2, int64_t sw3,
                                                            float *__restrict__ img) {
     const int64_t co_tiles = (CO + CT_BN - 1) / CT_BN, nkb = Kp / CT_BK;
     const int64_t total = co_tiles * nkb * CT_BN * CT_BK;
@@ -118,8 +119,9 @@ __global__ void __launch_bounds__(256) filter_image_kernel(const float *__restri
         const int64_t kb = (e / (CT_BK * CT_BN)) % nkb, ct = e / (CT_BK * CT_BN * nkb);
         const int64_t co = ct * CT_BN + n, k = kb * CT_BK + kk;
         float v = 0.0f;
-        if (co < CO && k < K) {
-            const int64_t rs = k / C, c = k % C, r = rs / S, s = rs % S;
+        const int64_t rs = k / Cp, c = k % Cp;
+        if (co < CO && k < K && c < C) {
+            const int64_t r = rs / S, s = rs % S;
             v = __ldg(w + co * sw0 + c * sw1 + r * sw2 + s * sw3);
         }
         const float h = rna_tf32(v);
