@@ -100,9 +100,28 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
     a.m_tiles = (int)((m_rows + tc::BM - 1) / tc::BM);
     a.n_tiles = (int)((n_rows + BN - 1) / BN);
     dim3 grid((unsigned)(a.m_tiles * a.n_tiles));
+    static long long *trace = nullptr;
+    const char *trace_path = getenv("LSB_GEMM_TRACE");
+    if (trace_path) {
+        if (!trace) cudaMalloc(&trace, 4 * 128 * sizeof(long long));
+        cudaMemsetAsync(trace, 0, 4 * 128 * sizeof(long long), s);
+        a.trace = trace;
+    }
     prof_mark(0, s);
     tc::tf32x3_gemm_kernel<BK, BN><<<grid, Cf::kThreads, Cf::kSmemBytes, s>>>(mah, mal, mbh, mbl, a);
     prof_mark(1, s);
+    if (trace_path) {
+        long long h[4 * 128];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
+        if (FILE *f = fopen(trace_path, "w")) {
+            for (int e = 0; e < 4; e++) {
+                for (int k = 0; k < 128; k++) fprintf(f, "%lld ", h[e * 128 + k]);
+                fprintf(f, "\n");
+            }
+            fclose(f);
+        }
+    }
     return LSB_OK;
 }
 
@@ -189,6 +208,26 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     a.M = M; a.N = N; a.K = K; a.Kp = Kp;
     a.C = C; a.sc_m = sc_m; a.sc_n = sc_n; a.c_vec = c_vec;
     a.epi = epi;
+    // fast epilogue when every stage is "(+ row-invariant operand[n]) then
+    // identity|ReLU" with beta 1 and no C_in (C4's bias + ReLU)
+    if (epi.n >= 1 && epi.n <= 2 && !getenv("LSB_NO_FAST_EPI")) {
+        bool ok = true;
+        for (int i = 0; i < epi.n && ok; i++) {
+            const lsb_epi_stage &st = epi.s[i];
+            ok = st.beta == 1.0f && st.alpha == 0.0f && (st.post == LSB_EW_IDENTITY || st.post == LSB_EW_RELU) &&
+                 (st.combine < 0 || (st.combine == LSB_OP_ADD && st.so[1] == 0 && st.operand != nullptr));
+            if (ok) {
+                a.fbias[i] = st.combine < 0 ? nullptr : st.operand;
+                a.fbias_stride[i] = st.so[2];
+                a.frelu[i] = st.post == LSB_EW_RELU;
+            }
+        }
+        if (ok) a.fast_n = epi.n;
+        else {
+            a.fbias[0] = a.fbias[1] = nullptr;
+            a.frelu[0] = a.frelu[1] = 0;
+        }
+    }
     return run_main_cfg(pick_cfg(N, K, epi.n > 0), ahi, alo, bhi, blo, M, N, Kp, a, s, err, errlen);
 }
 

@@ -148,4 +148,53 @@ __device__ __forceinline__ void apply_epilogue4(const EpiStages &e, float (&x)[4
     }
 }
 
+// GEMM-row variant of apply_epilogue4 (coordinates (0, m, n..n+3, 0)) whose
+// row-invariant operands (so[1] == 0: bias[n], column vectors) were loaded
+// once per column segment into pre[] by epi4_preload -- a per-row dependent
+// L2 round trip made the C4 epilogue 4x slower than its stores
+__device__ __forceinline__ void epi4_preload(const EpiStages &e, int64_t n, bool full4, float4 (&pre)[LSB_MAX_EPI]) {
+#pragma unroll
+    for (int i = 0; i < LSB_MAX_EPI; i++) {
+        pre[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i >= e.n) break;
+        const lsb_epi_stage &st = e.s[i];
+        if (st.combine >= 0 && st.so[1] == 0) {
+            if (full4) {
+                pre[i] = ldg4(st.operand, n * st.so[2], st.so[2]);
+            } else {
+                pre[i].x = __ldg(st.operand + n * st.so[2]);   // n < N always holds for the first
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void apply_epilogue4_pre(const EpiStages &e, float (&x)[4], int64_t m, int64_t n,
+                                                    const float4 (&pre)[LSB_MAX_EPI]) {
+#pragma unroll
+    for (int i = 0; i < LSB_MAX_EPI; i++) {
+        if (i >= e.n) break;
+        const lsb_epi_stage &st = e.s[i];
+        float t[4] = {x[0], x[1], x[2], x[3]};
+        if (st.combine >= 0) {
+            const float4 v = st.so[1] == 0 ? pre[i] : ldg4(st.operand, m * st.so[1] + n * st.so[2], st.so[2]);
+            t[0] = op_rt(st.combine, t[0], v.x);
+            t[1] = op_rt(st.combine, t[1], v.y);
+            t[2] = op_rt(st.combine, t[2], v.z);
+            t[3] = op_rt(st.combine, t[3], v.w);
+        }
+        if (st.beta != 1.0f) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) t[q] = __fmul_rn(st.beta, t[q]);
+        }
+        if (st.alpha != 0.0f) {
+            const float4 c = ldg4(st.c_in, m * st.sc[1] + n * st.sc[2], st.sc[2]);
+            const float cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int q = 0; q < 4; q++) t[q] = op_rt(st.reduce, __fmul_rn(st.alpha, ew_rt(st.pre, cv[q])), t[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) x[q] = ew_rt(st.post, t[q]);
+    }
+}
+
 }  // namespace lsb

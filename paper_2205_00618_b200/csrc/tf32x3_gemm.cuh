@@ -72,7 +72,27 @@ struct TcArgs {
     int64_t conv_hw, conv_wo;
     int64_t so[4];
     EpiStages epi;
+    // fast epilogue (fast_n stages, each "+ bias[n * stride]" if bias != null,
+    // then ReLU if relu): set by the host when every stage has that form
+    // (C4's bias + ReLU); the generic runtime-dispatched stage walk costs
+    // ~1k cycles per stored row (measured: 37k vs 8k cycles per 128x256 tile)
+    int fast_n;
+    const float *fbias[2];
+    int64_t fbias_stride[2];
+    int frelu[2];
+    long long *trace;     // debug (LSB_TC_TRACE builds): clock64 stamps of CTA 0
 };
+
+#ifdef LSB_TC_TRACE
+#define TC_TRACE(ev, i)                                                                \
+    do {                                                                               \
+        if (p.trace != nullptr && blockIdx.x == 0 && (i) < 128) p.trace[(ev) * 128 + (i)] = clock64(); \
+    } while (0)
+#else
+#define TC_TRACE(ev, i) \
+    do {                \
+    } while (0)
+#endif
 
 // ---------------------------------------------------------------- PTX wrappers
 
@@ -345,6 +365,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     const int64_t m0 = (int64_t)mt * BM, n0 = (int64_t)nt * BN;
     const int num_kb = (int)(p.Kp / BK);
     const int num_chunks = (num_kb + kChunkStages - 1) / kChunkStages;
+    if (threadIdx.x == 0) TC_TRACE(3, 0);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&map_ahi);
@@ -404,8 +425,10 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(b * BN);
                 const int kb_end = min(num_kb, (c + 1) * kChunkStages);
+                TC_TRACE(2, c);
                 for (int kb = c * kChunkStages; kb < kb_end; kb++) {
                     mbar_wait(&full[stage], phase);
+                    TC_TRACE(0, kb);
                     tc_fence_after();
                     const uint32_t base = smem_u32(smem + stage * kStageBytes);
                     const uint64_t ahi = sdesc_k_sw<Cf::kSwizzleBytes>(base);
@@ -441,6 +464,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
         for (int c = 0; c < num_chunks; c++) {
             const int b = c & 1;
             mbar_wait(&tfull[b], (uint32_t)((c >> 1) & 1));
+            if (warp == 2 && lane == 0) TC_TRACE(1, c);
             tc_fence_after();
 #pragma unroll
             for (int part = 0; part < 4; part++) {
@@ -465,9 +489,32 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
             *reinterpret_cast<float4 *>(tile + row * BN + pos * 4) =
                 make_float4(tot[c4 * 4], tot[c4 * 4 + 1], tot[c4 * 4 + 2], tot[c4 * 4 + 3]);
         }
+        if (warp == 2 && lane == 0) TC_TRACE(3, 1);
         asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");   // epilogue warps only
+        if (warp == 2 && lane == 0) TC_TRACE(3, 2);
         const int ew = warp - 2;
         constexpr int kRowsPerWarp = BM / kEpiWarps;
+        // row-invariant epilogue operands (bias[n]) once per column segment
+        float fpre[BN / 128][2][4];
+        if (p.fast_n) {
+#pragma unroll
+            for (int h = 0; h < BN / 128; h++) {
+                const int64_t n = n0 + (h * 32 + lane) * 4;
+#pragma unroll
+                for (int i = 0; i < 2; i++)
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        fpre[h][i][e] = (p.fbias[i] && n + e < p.N) ? __ldg(p.fbias[i] + (n + e) * p.fbias_stride[i]) : 0.f;
+            }
+        }
+        float4 pre[BN / 128][LSB_MAX_EPI];
+        if (p.epi.n && !p.fast_n && p.conv_hw == 0) {
+#pragma unroll
+            for (int h = 0; h < BN / 128; h++) {
+                const int64_t n = n0 + (h * 32 + lane) * 4;
+                if (n < p.N) epi4_preload(p.epi, n, n + 3 < p.N, pre[h]);
+            }
+        }
 #pragma unroll 1
         for (int rr = 0; rr < kRowsPerWarp; rr++) {
             const int r = ew * kRowsPerWarp + rr;
@@ -493,9 +540,19 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                     }
                     continue;
                 }
-                if (p.epi.n) {
+                if (p.fast_n) {
+#pragma unroll
+                    for (int i = 0; i < 2; i++) {
+                        if (i >= p.fast_n) break;
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            if (p.fbias[i]) x[e] += fpre[h][i][e];
+                            if (p.frelu[i]) x[e] = fmaxf(x[e], 0.0f);
+                        }
+                    }
+                } else if (p.epi.n) {
                     if (n + 3 < p.N) {
-                        apply_epilogue4(p.epi, x, 0, m, n, 0);
+                        apply_epilogue4_pre(p.epi, x, m, n, pre[h]);
                     } else {
 #pragma unroll
                         for (int e = 0; e < 4; e++)
@@ -513,8 +570,10 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
             }
         }
     }
+    if (warp == 2 && lane == 0) TC_TRACE(3, 3);
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) TC_TRACE(3, 4);
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::kTmemCols));
