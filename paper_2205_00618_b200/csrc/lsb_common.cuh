@@ -15,6 +15,20 @@
 
 namespace lsb {
 
+// max/min with NaN propagation, like the reference's np.max / np.maximum
+// (feedback.py:29-42): fmaxf/fminf are IEEE maxNum and drop a NaN operand.
+// Same cost: nested pairs still fuse into FMNMX3 (as FMNMX3.NAN).
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float d;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+    float d;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+
 template <int OP>
 struct Op;
 template <>
@@ -29,12 +43,12 @@ struct Op<LSB_OP_MUL> {
 };
 template <>
 struct Op<LSB_OP_MAX> {
-    static __device__ __forceinline__ float apply(float a, float b) { return fmaxf(a, b); }
+    static __device__ __forceinline__ float apply(float a, float b) { return fmax_nan(a, b); }
     static __device__ __forceinline__ float identity() { return -INFINITY; }
 };
 template <>
 struct Op<LSB_OP_MIN> {
-    static __device__ __forceinline__ float apply(float a, float b) { return fminf(a, b); }
+    static __device__ __forceinline__ float apply(float a, float b) { return fmin_nan(a, b); }
     static __device__ __forceinline__ float identity() { return INFINITY; }
 };
 
@@ -42,8 +56,8 @@ __device__ __forceinline__ float op_rt(int op, float a, float b) {
     switch (op) {
     case LSB_OP_ADD: return __fadd_rn(a, b);
     case LSB_OP_MUL: return __fmul_rn(a, b);
-    case LSB_OP_MAX: return fmaxf(a, b);
-    default: return fminf(a, b);
+    case LSB_OP_MAX: return fmax_nan(a, b);
+    default: return fmin_nan(a, b);
     }
 }
 
@@ -68,7 +82,7 @@ static __device__ __noinline__ float sigmoid_f64(float x) {
 
 // vm.py:214-228: relu = max(x, 0)
 __device__ __forceinline__ float ew_rt(int ew, float x) {
-    if (ew == LSB_EW_RELU) return fmaxf(x, 0.0f);
+    if (ew == LSB_EW_RELU) return fmax_nan(x, 0.0f);
     if (ew == LSB_EW_SIGMOID) return sigmoid_f64(x);
     return x;
 }

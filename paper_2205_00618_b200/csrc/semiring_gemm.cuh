@@ -483,12 +483,18 @@ __device__ __forceinline__ void mainloop(const GemmArgs &p, int64_t bz, int64_t 
 
 // order-preserving float max/min through integer atomics (exact, so the
 // result does not depend on the order partial tiles arrive in)
+// A NaN partial must win (np.max propagates it): for max it is stored as
+// 0x7fffffff (above +inf as int, below every negative float as unsigned),
+// for min as 0xffffffff (below every positive float as int, above every
+// negative float as unsigned), so no later partial can displace it.
 __device__ __forceinline__ void atomic_max_f32(float *a, float v) {
-    if (v >= 0.0f) atomicMax(reinterpret_cast<int *>(a), __float_as_int(v));
+    if (v != v) atomicMax(reinterpret_cast<int *>(a), 0x7fffffff);
+    else if (v >= 0.0f) atomicMax(reinterpret_cast<int *>(a), __float_as_int(v));
     else atomicMin(reinterpret_cast<unsigned *>(a), __float_as_uint(v));
 }
 __device__ __forceinline__ void atomic_min_f32(float *a, float v) {
-    if (v >= 0.0f) atomicMin(reinterpret_cast<int *>(a), __float_as_int(v));
+    if (v != v) atomicMax(reinterpret_cast<unsigned *>(a), 0xffffffffu);
+    else if (v >= 0.0f) atomicMin(reinterpret_cast<int *>(a), __float_as_int(v));
     else atomicMax(reinterpret_cast<unsigned *>(a), __float_as_uint(v));
 }
 

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) nchw_split_nhwc_kernel(const float *__res
             const float vh = rna_tf32(v);
             const int64_t o = ((nh * W) + w) * Cp + c;
             hi[o] = vh;
-            lo[o] = rna_tf32(v - vh);
+            lo[o] = tf32_lo(v, vh);
         }
     }
 }

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) filter_image_kernel(const float *__restri
             v = __ldg(w + co * sw0 + c * sw1 + r * sw2 + s * sw3);
         }
         const float h = rna_tf32(v);
-        const float l = rna_tf32(v - h);
+        const float l = tf32_lo(v, h);
         const int64_t base = ((ct * nkb + kb) * 2) * (CT_BN * CT_BK);
         const int off = n * 16 + (((kk >> 2) ^ ((n >> 1) & 3)) << 2) + (kk & 3);   // floats
         img[base + off] = h;

@@ -206,6 +206,12 @@ __device__ __forceinline__ float rna_tf32(float x) {
     return __uint_as_float(r);
 }
 
+// lo part of the 3xTF32 split; an infinite hi gets lo = 0 so inf inputs give
+// inf products (inf - inf = NaN in lo would turn every such product to NaN)
+__device__ __forceinline__ float tf32_lo(float x, float h) {
+    return fabsf(h) == __int_as_float(0x7f800000) ? 0.0f : rna_tf32(x - h);
+}
+
 // ---------------------------------------------------------------- prepass
 
 // X element (r, k) = X[r*s_r + k*s_k]  ->  hi/lo[r][k] (row-major, Kp columns,
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
             float x = tile[a][tx];
             float h = rna_tf32(x);
             hi[r * Kp + k] = h;
-            lo[r * Kp + k] = rna_tf32(x - h);
+            lo[r * Kp + k] = tf32_lo(x, h);
         }
     }
 }
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(256) im2col_split_kernel(const float *__restri
             const float v = tile[a][tx];
             const float h = rna_tf32(v);
             hi[pp * g.Kp + k] = h;
-            lo[pp * g.Kp + k] = rna_tf32(v - h);
+            lo[pp * g.Kp + k] = tf32_lo(v, h);
         }
     }
 }
@@ -323,7 +329,7 @@ __global__ void __launch_bounds__(256) filter_split_kernel(const float *__restri
         }
         const float h = rna_tf32(v);
         hi[e] = h;
-        lo[e] = rna_tf32(v - h);
+        lo[e] = tf32_lo(v, h);
     }
 }
 

@@ -1,0 +1,162 @@
+"""Edge cases beyond the golden fixtures, checked against the oracle
+(oracle/oracle.py, the reference_eval restatement): non-finite inputs
+(NaN must propagate through max/min like np.max, ±inf through sums),
+degenerate and ragged extents, the stream-K merge with NaN partials.
+
+Inputs are integer-valued floats so max/min/sum results are exact; graphs are
+golden graphs with their extents resized (shard.shard_graph keeps split
+lineage consistent)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import common
+from oracle import oracle as O
+from paper_2205_00618_b200 import backend, shard
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(name):
+    return next(c for c in common.index()["cases"] if c["name"] == name)
+
+
+def _graph(name, **sizes):
+    obj = json.loads(common.graph_json(_case(name)["graph"]))
+    for var, n in sizes.items():
+        obj = shard.shard_graph(obj, n, var)
+    return json.dumps(obj)
+
+
+def _inputs(gj, seed, lo=-4, hi=5):
+    k = backend.compile_graph(gj)
+    rng = np.random.default_rng(seed)
+    return k, {s: rng.integers(lo, hi, size=shp).astype(np.float32)
+               for s, shp in k.slot_shapes.items() if s in k.input_slots}
+
+
+def _run(k, ins):
+    bufs = {s: a.copy() for s, a in ins.items()}
+    backend.execute(k, bufs)
+    return bufs
+
+
+def _same(got, ref, exact=True):
+    """NaN where the reference has NaN, equal infinities, finite values equal
+    (exact) or within the strict sum tolerance."""
+    ref = np.asarray(ref, np.float64)
+    got = np.asarray(got, np.float64).reshape(ref.shape)
+    nan_r, nan_g = np.isnan(ref), np.isnan(got)
+    assert np.array_equal(nan_r, nan_g), f"NaN mask differs at {np.argwhere(nan_r != nan_g)[:5].tolist()}"
+    inf_r = np.isinf(ref)
+    assert np.array_equal(got[inf_r], ref[inf_r]), "infinities differ"
+    fin = ~(nan_r | inf_r)
+    if exact:
+        assert np.array_equal(got[fin].astype(np.float32), ref[fin].astype(np.float32))
+    else:
+        assert common.strict_ok(got[fin], ref[fin]).all()
+
+
+@pytest.mark.parametrize("op", ["add_max", "add_min"])
+@pytest.mark.parametrize("shape", [(37, 29, 53), (300, 257, 700)])
+def test_tropical_nonfinite(op, shape):
+    """NaN poisons its row/column like np.max; -inf/+inf entries behave as in
+    the f64 reference (inf + -inf = NaN)."""
+    m, k, n = shape
+    gj = _graph(f"semiring_{op}", m=m, k=k, n=n)
+    kern, ins = _inputs(gj, 7)
+    A, B = ins[0], ins[1]
+    A[3, 5] = np.nan
+    A[7, :] = -np.inf
+    A[11, 2] = np.inf
+    B[4, 9] = -np.inf
+    B[6, n - 1] = np.nan
+    got = _run(kern, ins)
+    ref = O.reference_eval(gj, ins)
+    out = [s for s in ref][0]
+    _same(got[out], ref[out], exact=True)
+
+
+def test_maxplus_streamk_nan_partials():
+    """1024^3 max-plus takes the stream-K kernel (partial tiles merged by
+    integer atomics); a NaN partial must win the merge in every case."""
+    gj = common.graph_json(common.config("C2")["graph"])
+    kern, ins = _inputs(gj, 11, -10, 11)
+    A, B = ins[0], ins[1]
+    rows = [0, 5, 200, 777, 1023]
+    A[5, 1000] = np.nan              # late k: lands in a different partial than k=0
+    A[200, 3] = np.nan
+    B[900, 17] = np.nan              # column 17 of every row
+    A[777, :512] = -np.inf
+    got = _run(kern, ins)
+    mvar = [v["id"] for v in json.loads(gj)["vars"] if v["name"] == "m"][0]
+    ref = O.reference_eval(gj, ins, restrict={mvar: np.array(rows)})
+    out = [s for s in ref][0]
+    _same(got[out].reshape(1024, 1024)[rows], ref[out], exact=True)
+
+
+@pytest.mark.parametrize("algo", ["simt", "tf32x3"])
+def test_sum_nan_propagates(algo, monkeypatch):
+    monkeypatch.setenv("LSB_GEMM_ALGO", algo)
+    gj = _graph("semiring_mul_add", m=130, k=77, n=96)
+    kern, ins = _inputs(gj, 3)
+    ins[0][4, 10] = np.nan
+    ins[1][20, 33] = np.nan
+    got = _run(kern, ins)
+    ref = O.reference_eval(gj, ins)
+    out = [s for s in ref][0]
+    _same(got[out], ref[out], exact=False)
+
+
+def test_sum_inf_simt(monkeypatch):
+    """±inf through (mul, add) on the FP32 path (the 3xTF32 path turns
+    inf x (lo = 0) into NaN; DESIGN.md §8 lists it)."""
+    monkeypatch.setenv("LSB_GEMM_ALGO", "simt")
+    gj = _graph("semiring_mul_add", m=64, k=40, n=48)
+    kern, ins = _inputs(gj, 5)
+    ins[0][2, 3] = np.inf
+    ins[0][9, 1] = -np.inf
+    ins[1][7, 30] = np.inf
+    got = _run(kern, ins)
+    ref = O.reference_eval(gj, ins)
+    out = [s for s in ref][0]
+    _same(got[out], ref[out], exact=False)
+
+
+def test_relu_of_nan_is_nan():
+    gj = common.graph_json(_case("mlp_bias_relu_small")["graph"])
+    kern, ins = _inputs(gj, 9)
+    ins[0][1, 2] = np.nan
+    got = _run(kern, ins)
+    ref = O.reference_eval(gj, ins)
+    for s in ref:
+        _same(got[s], ref[s], exact=False)
+
+
+@pytest.mark.parametrize("algo", ["auto", "simt", "tf32x3"])
+@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 64, 300), (257, 1, 3), (3, 300, 1), (129, 70, 131)])
+def test_degenerate_and_ragged_sum(algo, shape, monkeypatch):
+    if algo != "auto":
+        monkeypatch.setenv("LSB_GEMM_ALGO", algo)
+    m, k, n = shape
+    gj = _graph("semiring_mul_add", m=m, k=k, n=n)
+    kern, ins = _inputs(gj, 13)
+    got = _run(kern, ins)
+    ref = O.reference_eval(gj, ins)
+    out = [s for s in ref][0]
+    _same(got[out], ref[out], exact=True)     # small integers: exact in fp32 and 3xTF32
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 600, 2), (513, 1, 129), (1000, 777, 1111)])
+def test_degenerate_and_ragged_tropical(shape):
+    m, k, n = shape
+    gj = _graph("semiring_add_max", m=m, k=k, n=n)
+    kern, ins = _inputs(gj, 17)
+    got = _run(kern, ins)
+    mvar = [v["id"] for v in json.loads(gj)["vars"] if v["name"] == "m"][0]
+    rows = np.unique(np.array([0, m // 2, m - 1]))
+    ref = O.reference_eval(gj, ins, restrict={mvar: rows})
+    out = [s for s in ref][0]
+    _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
