@@ -35,6 +35,12 @@ struct BKey {
     }
 };
 BKey g_bkey;
+// non-finite row flags (TcArgs::rowflag/colflag): generation-stamped, so no
+// per-call reset; zeroed only when (re)allocated
+int *g_flags = nullptr;
+int64_t g_flags_n = 0;
+int g_gen = 0, g_bgen = 0;
+int *g_conv_flag = nullptr;   // the NHWC conv's "non-finite input" flag (generation-stamped)
 
 bool load_encode() {
     if (g_encode) return true;
@@ -194,12 +200,42 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
         g_bkey = key;
     }
     float *bhi = ws, *blo = bhi + N * Kp, *ahi = blo + N * Kp, *alo = ahi + M * Kp;
+    int *colflag, *rowflag, *anyflag, *done, agen, bgen;
+    {
+        std::lock_guard<std::mutex> lk(g_tc_mu);
+        if (M + N + 4 > g_flags_n) {
+            if (g_flags) {
+                cudaDeviceSynchronize();
+                cudaFree(g_flags);
+            }
+            g_flags = nullptr;
+            g_flags_n = 0;
+            if (cudaMalloc(&g_flags, sizeof(int) * (size_t)(M + N + 4)) != cudaSuccess) {
+                snprintf(err, errlen, "cudaMalloc of the non-finite flags failed");
+                return LSB_ERR_NOMEM;
+            }
+            cudaMemsetAsync(g_flags, 0, sizeof(int) * (size_t)(M + N + 4), s);
+            g_flags_n = M + N + 4;
+            reuse_b = false;   // B's flags were lost
+            g_bkey = BKey{};
+        }
+        // [anyA, anyB, done, pad | colflag[N] | rowflag[M]]
+        anyflag = g_flags;
+        done = g_flags + 2;
+        colflag = g_flags + 4;
+        rowflag = colflag + N;
+        agen = ++g_gen;
+        if (agen <= 0) agen = g_gen = 1;   // (2^31 calls) never 0, the zeroed state
+        if (!reuse_b) g_bgen = agen;
+        bgen = g_bgen;
+    }
     {
         dim3 ga((unsigned)((Kp + 31) / 32), (unsigned)((M + 31) / 32));
-        tc::tf32_split_kernel<<<ga, 256, 0, s>>>(A, M, K, sa_m, sa_k, ahi, alo, Kp);
+        tc::tf32_split_kernel<<<ga, 256, 0, s>>>(A, M, K, sa_m, sa_k, ahi, alo, Kp, rowflag, anyflag, agen);
         if (!reuse_b) {
             dim3 gb((unsigned)((Kp + 31) / 32), (unsigned)((N + 31) / 32));
-            tc::tf32_split_kernel<<<gb, 256, 0, s>>>(B, N, K, sb_n, sb_k, bhi, blo, Kp);
+            tc::tf32_split_kernel<<<gb, 256, 0, s>>>(B, N, K, sb_n, sb_k, bhi, blo, Kp, colflag, anyflag + 1,
+                                                     bgen);
         }
         if (aux_launches) *aux_launches = reuse_b ? 1 : 2;
     }
@@ -208,6 +244,8 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     a.M = M; a.N = N; a.K = K; a.Kp = Kp;
     a.C = C; a.sc_m = sc_m; a.sc_n = sc_n; a.c_vec = c_vec;
     a.epi = epi;
+    a.rowflag = rowflag; a.colflag = colflag; a.anyflag = anyflag; a.done = done; a.agen = agen; a.bgen = bgen;
+    a.ahi = ahi; a.alo = alo; a.bhi = bhi; a.blo = blo;
     // fast epilogue when every stage is "(+ row-invariant operand[n]) then
     // identity|ReLU" with beta 1 and no C_in (C4's bias + ReLU)
     if (epi.n >= 1 && epi.n <= 2 && !getenv("LSB_NO_FAST_EPI")) {
@@ -411,7 +449,7 @@ int tf32x3_conv_tma(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_l
     const int64_t co_tiles = (CO + tc::CT_BN - 1) / tc::CT_BN;
     const int64_t wtot = co_tiles * Kp * tc::CT_BN;
     tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
-        c.w, CO, K, Kp, c.C, c.C, c.S, c.sw0, c.sw1, c.sw2, c.sw3, ws);
+        c.w, CO, K, Kp, c.C, c.C, c.S, c.sw0, c.sw1, c.sw2, c.sw3, ws, nullptr, 0);
     if (aux_launches) *aux_launches = 1;
     CUtensorMap mx;
     {
@@ -503,12 +541,27 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
     float *ws = acquire_ws(sizeof(float) * (2 * xel + wel), err, errlen);
     if (!ws) return LSB_ERR_NOMEM;
     float *xhi = ws, *xlo = xhi + xel, *wimg = xlo + xel;
+    int *anyflag, gen;
+    {
+        std::lock_guard<std::mutex> lk(g_tc_mu);
+        if (!g_conv_flag) {
+            if (cudaMalloc(&g_conv_flag, sizeof(int)) != cudaSuccess) {
+                snprintf(err, errlen, "cudaMalloc of the non-finite flag failed");
+                return LSB_ERR_NOMEM;
+            }
+            cudaMemsetAsync(g_conv_flag, 0, sizeof(int), s);
+        }
+        anyflag = g_conv_flag;
+        gen = ++g_gen;
+        if (gen <= 0) gen = g_gen = 1;
+    }
     {
         dim3 g((unsigned)((c.W + 31) / 32), (unsigned)((Cp + 31) / 32), (unsigned)(n_img * c.H));
-        tc::nchw_split_nhwc_kernel<<<g, 256, 0, s>>>(c.x, c.C, c.H, c.W, Cp, c.sx0, c.sx1, c.sx2, c.sx3, xhi, xlo);
+        tc::nchw_split_nhwc_kernel<<<g, 256, 0, s>>>(c.x, c.C, c.H, c.W, Cp, c.sx0, c.sx1, c.sx2, c.sx3, xhi, xlo,
+                                                     anyflag, gen);
         const int64_t wtot = co_tiles * tc::CN_BN * K;
         tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
-            c.w, CO, K, K, c.C, Cp, c.S, c.sw0, c.sw1, c.sw2, c.sw3, wimg);
+            c.w, CO, K, K, c.C, Cp, c.S, c.sw0, c.sw1, c.sw2, c.sw3, wimg, anyflag, gen);
         if (aux_launches) *aux_launches = 2;
     }
     CUtensorMap mh, ml;
@@ -545,6 +598,13 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
     a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
     const int num_kb = (int)(K / tc::CN_BK);
     a.stages_per_chunk = (num_kb + tc::CN_CHUNKS - 1) / tc::CN_CHUNKS;
+    a.anyflag = anyflag;
+    a.gen = gen;
+    a.x = c.x;
+    a.w = c.w;
+    a.C = c.C; a.H = c.H; a.W = c.W;
+    a.sx[0] = c.sx0; a.sx[1] = c.sx1; a.sx[2] = c.sx2; a.sx[3] = c.sx3;
+    a.swt[0] = c.sw0; a.swt[1] = c.sw1; a.swt[2] = c.sw2; a.swt[3] = c.sw3;
     a.vec4 = c.WO % 4 == 0 && c.so3 == 1 && c.so2 % 4 == 0 && c.so1 % 4 == 0 && c.so0 % 4 == 0 &&
              reinterpret_cast<uintptr_t>(c.o) % 16 == 0;
     a.epi = c.epi;

@@ -45,6 +45,13 @@ struct ConvNhwcArgs {
     int64_t so[4];
     int stages_per_chunk;
     int vec4;             // float4 output stores (see the epilogue)
+    // non-finite inputs (flagged by the prepasses: *anyflag == gen): the
+    // tile is recomputed in FP32 from the original X and W in the epilogue
+    // (3xTF32 would turn inf x (lo = 0) into NaN)
+    const int *anyflag;
+    int gen;
+    const float *x, *w;
+    int64_t C, H, W, sx[4], swt[4];
     EpiStages epi;
     long long *trace;     // debug (LSB_CN_TRACE builds): per-stage clock64 stamps of CTA 0
 };
@@ -66,7 +73,8 @@ struct ConvNhwcArgs {
 __global__ void __launch_bounds__(256) nchw_split_nhwc_kernel(const float *__restrict__ x, int64_t C, int64_t H,
                                                               int64_t W, int64_t Cp, int64_t sx0, int64_t sx1,
                                                               int64_t sx2, int64_t sx3, float *__restrict__ hi,
-                                                              float *__restrict__ lo) {
+                                                              float *__restrict__ lo, int *__restrict__ any,
+                                                              int gen) {
     __shared__ float tile[32][33];
     const int64_t nh = blockIdx.z;   // n * H + h
     const int64_t n = nh / H, h = nh % H;
@@ -89,6 +97,7 @@ __global__ void __launch_bounds__(256) nchw_split_nhwc_kernel(const float *__res
             const int64_t o = ((nh * W) + w) * Cp + c;
             hi[o] = vh;
             lo[o] = tf32_lo(v, vh);
+            if (!(fabsf(v) < __int_as_float(0x7f800000))) *any = gen;
         }
     }
 }
@@ -234,6 +243,30 @@ __global__ void __launch_bounds__(CN_THREADS, 2)
         tc_fence_before();
         asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
         if (ew == 0 && lane == 0) CN_TRACE(2, 4);
+        if (*p.anyflag == p.gen) {
+            // non-finite input somewhere: FP32 recompute of this tile's outputs
+            asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
+            for (int i = threadIdx.x - 64; i < CN_BN * 128; i += CN_EPI_WARPS * 32) {
+                const int co_l = i / 128, pix = i % 128, ho = h0 + pix / 32, wo = w0 + pix % 32;
+                const int64_t co = c0 + co_l;
+                if (co >= p.CO || ho >= p.HO || wo >= p.WO) continue;
+                float acc = 0.0f;
+                // out-of-range taps contribute fill (0) x w, as the reference's
+                // guarded view does: inf x 0 = NaN must appear there too
+                for (int64_t c = 0; c < p.C; c++)
+                    for (int64_t r = 0; r < p.R; r++) {
+                        const int64_t hi_ = ho * p.sh - p.ph + r * p.dh;
+                        for (int64_t s2 = 0; s2 < p.S; s2++) {
+                            const int64_t wi = wo * p.sw - p.pw + s2 * p.dw;
+                            const bool in = hi_ >= 0 && hi_ < p.H && wi >= 0 && wi < p.W;
+                            const float xv = in ? p.x[n * p.sx[0] + c * p.sx[1] + hi_ * p.sx[2] + wi * p.sx[3]] : 0.0f;
+                            acc = fmaf(xv, p.w[co * p.swt[0] + c * p.swt[1] + r * p.swt[2] + s2 * p.swt[3]], acc);
+                        }
+                    }
+                tile[co_l * 128 + pix] = acc;
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
+        }
         if (p.vec4) {
             // one float4 per lane: lane -> output row h = lane / 8, columns
             // w0 + 4 (lane % 8) .. +3; a warp stores one channel's 4 x 32 tile

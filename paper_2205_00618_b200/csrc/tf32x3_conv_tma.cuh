@@ -110,7 +110,7 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 __global__ void __launch_bounds__(256) filter_image_kernel(const float *__restrict__ w, int64_t CO, int64_t K,
                                                            int64_t Kp, int64_t C, int64_t Cp, int64_t S,
                                                            int64_t sw0, int64_t sw1, int64_t sw2, int64_t sw3,
-                                                           float *__restrict__ img) {
+                                                           float *__restrict__ img, int *__restrict__ any, int gen) {
     const int64_t co_tiles = (CO + CT_BN - 1) / CT_BN, nkb = Kp / CT_BK;
     const int64_t total = co_tiles * nkb * CT_BN * CT_BK;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(256) filter_image_kernel(const float *__restri
         }
         const float h = rna_tf32(v);
         const float l = tf32_lo(v, h);
+        if (any != nullptr && !(fabsf(v) < __int_as_float(0x7f800000))) *any = gen;
         const int64_t base = ((ct * nkb + kb) * 2) * (CT_BN * CT_BK);
         const int off = n * 16 + (((kk >> 2) ^ ((n >> 1) & 3)) << 2) + (kk & 3);   // floats
         img[base + off] = h;

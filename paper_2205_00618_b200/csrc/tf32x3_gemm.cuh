@@ -80,6 +80,15 @@ struct TcArgs {
     const float *fbias[2];
     int64_t fbias_stride[2];
     int frelu[2];
+    // non-finite inputs: 3xTF32 turns inf x (lo = 0) into NaN, so outputs in
+    // an A row / B column holding inf or NaN (rowflag[m] == agen, colflag[n]
+    // == bgen, written by the split prepass) are recomputed in FP32 from the
+    // split operands (hi + lo == x exactly for non-finite x) -- IEEE results
+    // like the reference's f64 evaluation; never taken for finite inputs
+    const int *rowflag, *colflag, *anyflag;   // anyflag[0] A, [1] B
+    int *done;                                 // CTA completion counter
+    int agen, bgen;
+    const float *ahi, *alo, *bhi, *blo;
     long long *trace;     // debug (LSB_TC_TRACE builds): clock64 stamps of CTA 0
 };
 
@@ -217,9 +226,11 @@ __device__ __forceinline__ float tf32_lo(float x, float h) {
 // X element (r, k) = X[r*s_r + k*s_k]  ->  hi/lo[r][k] (row-major, Kp columns,
 // zero padded).  32x32 tiles through smem so both the read (whichever stride
 // is 1) and the write (k fastest) are coalesced.
+// A row holding a non-finite value gets flag[r] = gen (see TcArgs::rowflag).
 __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict__ X, int64_t R, int64_t Kd,
                                                          int64_t s_r, int64_t s_k, float *__restrict__ hi,
-                                                         float *__restrict__ lo, int64_t Kp) {
+                                                         float *__restrict__ lo, int64_t Kp,
+                                                         int *__restrict__ flag, int *__restrict__ any, int gen) {
     __shared__ float tile[32][33];
     const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
@@ -242,6 +253,10 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
             float h = rna_tf32(x);
             hi[r * Kp + k] = h;
             lo[r * Kp + k] = tf32_lo(x, h);
+            if (flag != nullptr && !(fabsf(x) < __int_as_float(0x7f800000))) {
+                flag[r] = gen;
+                *any = gen;
+            }
         }
     }
 }
@@ -331,6 +346,42 @@ __global__ void __launch_bounds__(256) filter_split_kernel(const float *__restri
         hi[e] = h;
         lo[e] = tf32_lo(v, h);
     }
+}
+
+// Non-finite fixup, run by the last CTA to finish (so every tile is stored):
+// outputs of flagged A rows / B columns recomputed in FP32 from the split
+// operands, epilogue applied.  One flag load per operand when nothing was
+// flagged; the done counter is re-armed for the next launch.
+__device__ void tc_nonfinite_fixup(const TcArgs &p) {
+    // the split prepass finished before this grid started: when it flagged
+    // nothing (the normal case) every CTA leaves here, no fence, no atomic
+    const bool fa = p.anyflag[0] == p.agen, fb = p.anyflag[1] == p.bgen;
+    if (!fa && !fb) return;
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(p.done, 1) == (int)(gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    auto fix = [&](int64_t m, int64_t n) {
+        const float *ah = p.ahi + m * p.Kp, *al = p.alo + m * p.Kp, *bh = p.bhi + n * p.Kp, *bl = p.blo + n * p.Kp;
+        float acc = 0.0f;
+        for (int64_t k = 0; k < p.K; k++) acc = fmaf(ah[k] + al[k], bh[k] + bl[k], acc);
+        if (p.epi.n) acc = apply_epilogue(p.epi, acc, 0, m, n, 0);
+        p.C[m * p.sc_m + n * p.sc_n] = acc;
+    };
+    if (fa)
+        for (int64_t m = 0; m < p.M; m++)
+            if (p.rowflag[m] == p.agen)
+                for (int64_t n = threadIdx.x; n < p.N; n += blockDim.x) fix(m, n);
+    if (fb)
+        for (int64_t n = 0; n < p.N; n++)
+            if (p.colflag[n] == p.bgen)
+                for (int64_t m = threadIdx.x; m < p.M; m += blockDim.x) fix(m, n);
+    if (threadIdx.x == 0) *p.done = 0;
 }
 
 // ---------------------------------------------------------------- main kernel
@@ -533,6 +584,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 float4 v = *reinterpret_cast<const float4 *>(tile + r * BN + pos * 4);
                 const int64_t n = n0 + chunk * 4;
                 float x[4] = {v.x, v.y, v.z, v.w};
+
                 if (p.conv_hw > 0) {
 #pragma unroll
                     for (int e = 0; e < 4; e++) {
@@ -584,6 +636,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::kTmemCols));
     }
+    if (p.done != nullptr) tc_nonfinite_fixup(p);
 }
 
 }  // namespace tc

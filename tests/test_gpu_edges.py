@@ -110,10 +110,12 @@ def test_sum_nan_propagates(algo, monkeypatch):
     _same(got[out], ref[out], exact=False)
 
 
-def test_sum_inf_simt(monkeypatch):
-    """±inf through (mul, add) on the FP32 path (the 3xTF32 path turns
-    inf x (lo = 0) into NaN; DESIGN.md §8 lists it)."""
-    monkeypatch.setenv("LSB_GEMM_ALGO", "simt")
+@pytest.mark.parametrize("algo", ["simt", "tf32x3"])
+def test_sum_inf(algo, monkeypatch):
+    """±inf through (mul, add): exact IEEE on the FP32 path; on the 3xTF32
+    path the split prepass flags the rows/columns and those outputs are
+    recomputed in FP32 (inf x (lo = 0) would otherwise give NaN)."""
+    monkeypatch.setenv("LSB_GEMM_ALGO", algo)
     gj = _graph("semiring_mul_add", m=64, k=40, n=48)
     kern, ins = _inputs(gj, 5)
     ins[0][2, 3] = np.inf
@@ -160,3 +162,34 @@ def test_degenerate_and_ragged_tropical(shape):
     ref = O.reference_eval(gj, ins, restrict={mvar: rows})
     out = [s for s in ref][0]
     _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
+
+
+def test_tf32x3_inf_with_bias_relu_epilogue(monkeypatch):
+    monkeypatch.setenv("LSB_GEMM_ALGO", "tf32x3")
+    gj = common.graph_json(_case("mlp_bias_relu_small")["graph"])
+    kern, ins = _inputs(gj, 21)
+    ins[0][0, 1] = np.inf
+    ins[0][3, 0] = -np.inf
+    ins[1][2, 5] = np.inf
+    got = _run(kern, ins)
+    ref = O.reference_eval(gj, ins)
+    for s in ref:
+        _same(got[s], ref[s], exact=False)
+
+
+@pytest.mark.parametrize("algo", ["simt", "tf32x3"])
+def test_conv_nonfinite(algo, monkeypatch):
+    """inf/NaN in X and W through the conv paths; on the tensor-core path the
+    prepass flags them and the tile is recomputed in FP32."""
+    monkeypatch.setenv("LSB_GEMM_ALGO", algo)
+    gj = common.graph_json(_case("conv_pad1_small")["graph"])
+    kern, ins = _inputs(gj, 23)
+    x, w = ins[0], ins[1]
+    x.reshape(-1)[5] = np.inf
+    x.reshape(-1)[77] = -np.inf
+    x.reshape(-1)[130] = np.nan
+    w.reshape(-1)[3] = np.inf
+    got = _run(kern, ins)
+    ref = O.reference_eval(gj, ins)
+    for s in ref:
+        _same(got[s], ref[s], exact=False)
