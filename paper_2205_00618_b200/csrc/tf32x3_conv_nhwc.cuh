@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(256) nchw_split_nhwc_kernel(const float *__res
                                                               int64_t sx2, int64_t sx3, float *__restrict__ hi,
                                                               float *__restrict__ lo, int *__restrict__ any,
                                                               int gen) {
+    asm volatile("griddepcontrol.launch_dependents;");
     __shared__ float tile[32][33];
     const int64_t nh = blockIdx.z;   // n * H + h
     const int64_t n = nh / H, h = nh % H;
@@ -124,6 +125,10 @@ __global__ void __launch_bounds__(CN_THREADS, 2)
     const int cblocks = (int)(p.Cp / CN_BK);
     const int num_kb = (int)(p.R * p.S) * cblocks;
     if (threadIdx.x == 0) CN_TRACE(2, 2);
+#ifdef LSB_CN_TRACE
+    long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&map_hi);
@@ -148,6 +153,9 @@ __global__ void __launch_bounds__(CN_THREADS, 2)
     if (warp == 0) {
         // ---------------- TMA producer
         if (lane == 0) {
+            // launched with programmatic stream serialization: everything above
+            // overlapped the prepasses; their outputs are read from here on
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             const int hin0 = (int)(h0 * p.sh - p.ph), win0 = (int)(w0 * p.sw - p.pw);
             int stage = 0;
             uint32_t phase = 0;
@@ -209,6 +217,7 @@ __global__ void __launch_bounds__(CN_THREADS, 2)
     } else {
         // ---------------- epilogue (warps 2..9)
         const int ew = warp - 2;
+        asm volatile("griddepcontrol.wait;" ::: "memory");   // anyflag below is a prepass output
         mbar_wait(tdone, 0);
         if (ew == 0 && lane == 0) CN_TRACE(2, 0);
         tc_fence_after();
@@ -308,6 +317,16 @@ __global__ void __launch_bounds__(CN_THREADS, 2)
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) CN_TRACE(2, 1);
+#ifdef LSB_CN_TRACE
+    if (threadIdx.x == 0 && p.trace != nullptr) {
+        long long t_end;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        long long *c = p.trace + 3 * 64 + 3 * (blockIdx.x + gridDim.x * blockIdx.y);
+        c[0] = t_start; c[1] = t_end; c[2] = smid;
+    }
+#endif
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CN_CHUNKS * CN_ACC_COLS));

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(256) filter_image_kernel(const float *__restri
                                                            int64_t Kp, int64_t C, int64_t Cp, int64_t S,
                                                            int64_t sw0, int64_t sw1, int64_t sw2, int64_t sw3,
                                                            float *__restrict__ img, int *__restrict__ any, int gen) {
+    asm volatile("griddepcontrol.launch_dependents;");
     const int64_t co_tiles = (CO + CT_BN - 1) / CT_BN, nkb = Kp / CT_BK;
     const int64_t total = co_tiles * nkb * CT_BN * CT_BK;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;

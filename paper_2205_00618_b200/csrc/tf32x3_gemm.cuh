@@ -261,6 +261,75 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
     }
 }
 
+// Vectorised forms of tf32_split_kernel (the prepass moves 12 bytes per
+// element, so it runs at copy speed only with 16-B accesses and 32-bit index
+// math; the scalar kernel above reached ~half of it on C4):
+//  * k contiguous (s_k == 1): no transpose, one float4 in, one float4 out per
+//    plane; columns [Kd, Kp) written as zeros
+//  * r contiguous (s_r == 1): 32 x 32 tiles transposed through smem with
+//    float4 reads along r and float4 writes along k
+// Preconditions (checked by the host): 16-B aligned X, the contiguous extent
+// and the other stride multiples of 4, every index < 2^31.
+__global__ void __launch_bounds__(256) tf32_split_kcontig_kernel(const float *__restrict__ X, int R, int Kd, int s_r,
+                                                                 float *__restrict__ hi, float *__restrict__ lo,
+                                                                 int Kp, int *__restrict__ flag,
+                                                                 int *__restrict__ any, int gen) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int q4 = Kp / 4;
+    const int total = R * q4;
+    const float inf = __int_as_float(0x7f800000);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int r = e / q4, k = (e - r * q4) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < Kd) v = __ldg(reinterpret_cast<const float4 *>(X + (int64_t)r * s_r + k));
+        const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+        const int64_t o = (int64_t)r * Kp + k;
+        *reinterpret_cast<float4 *>(hi + o) = h;
+        *reinterpret_cast<float4 *>(lo + o) =
+            make_float4(tf32_lo(v.x, h.x), tf32_lo(v.y, h.y), tf32_lo(v.z, h.z), tf32_lo(v.w, h.w));
+        if (flag != nullptr && !(fabsf(v.x) < inf && fabsf(v.y) < inf && fabsf(v.z) < inf && fabsf(v.w) < inf)) {
+            flag[r] = gen;
+            *any = gen;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) tf32_split_rcontig_kernel(const float *__restrict__ X, int R, int Kd, int s_k,
+                                                                 float *__restrict__ hi, float *__restrict__ lo,
+                                                                 int Kp, int *__restrict__ flag,
+                                                                 int *__restrict__ any, int gen) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    __shared__ float tile[32][33];   // [k][r]
+    const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+    const int t = threadIdx.x;
+    {
+        const int kk = t >> 3, r4 = (t & 7) * 4;   // 32 k rows x 8 float4 along r
+        const int k = k0 + kk, r = r0 + r4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < Kd && r < R) v = __ldg(reinterpret_cast<const float4 *>(X + (int64_t)k * s_k + r));
+        tile[kk][r4] = v.x;
+        tile[kk][r4 + 1] = v.y;
+        tile[kk][r4 + 2] = v.z;
+        tile[kk][r4 + 3] = v.w;
+    }
+    __syncthreads();
+    const int rr = t >> 3, k4 = (t & 7) * 4;       // 32 r rows x 8 float4 along k
+    const int r = r0 + rr, k = k0 + k4;
+    if (r < R && k < Kp) {
+        const float4 v = make_float4(tile[k4][rr], tile[k4 + 1][rr], tile[k4 + 2][rr], tile[k4 + 3][rr]);
+        const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+        const int64_t o = (int64_t)r * Kp + k;
+        *reinterpret_cast<float4 *>(hi + o) = h;
+        *reinterpret_cast<float4 *>(lo + o) =
+            make_float4(tf32_lo(v.x, h.x), tf32_lo(v.y, h.y), tf32_lo(v.z, h.z), tf32_lo(v.w, h.w));
+        const float inf = __int_as_float(0x7f800000);
+        if (flag != nullptr && !(fabsf(v.x) < inf && fabsf(v.y) < inf && fabsf(v.z) < inf && fabsf(v.w) < inf)) {
+            flag[r] = gen;
+            *any = gen;
+        }
+    }
+}
+
 // Conv prepass: im2col + split of the input.  Row p = output pixel
 // (img, ho, wo), column k = tap (c, r, s); out-of-range taps take the view's
 // oob `fill`.  32 pixels x 32 taps per block: read with pixels fastest (wo
@@ -353,8 +422,10 @@ __global__ void __launch_bounds__(256) filter_split_kernel(const float *__restri
 // operands, epilogue applied.  One flag load per operand when nothing was
 // flagged; the done counter is re-armed for the next launch.
 __device__ void tc_nonfinite_fixup(const TcArgs &p) {
-    // the split prepass finished before this grid started: when it flagged
-    // nothing (the normal case) every CTA leaves here, no fence, no atomic
+    // the split prepass has finished (and is visible) once griddepcontrol.wait
+    // returns; when it flagged nothing (the normal case) every CTA leaves
+    // here, no fence, no atomic
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const bool fa = p.anyflag[0] == p.agen, fb = p.anyflag[1] == p.bgen;
     if (!fa && !fb) return;
     __shared__ int s_last;
@@ -452,6 +523,9 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     if (warp == 0) {
         // ---------------- TMA producer
         if (lane == 0) {
+            // programmatic dependent launch: the setup above overlapped the
+            // split prepass; its outputs are read from here on
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             int stage = 0;
             uint32_t phase = 0;
             for (int kb = 0; kb < num_kb; kb++) {
