@@ -586,8 +586,16 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
     }
     {
         dim3 g((unsigned)((c.W + 31) / 32), (unsigned)((Cp + 31) / 32), (unsigned)(n_img * c.H));
-        tc::nchw_split_nhwc_kernel<<<g, 256, 0, s>>>(c.x, c.C, c.H, c.W, Cp, c.sx0, c.sx1, c.sx2, c.sx3, xhi, xlo,
-                                                     anyflag, gen);
+        const bool vec = c.sx3 == 1 && c.W % 4 == 0 && c.sx0 % 4 == 0 && c.sx1 % 4 == 0 && c.sx2 % 4 == 0 &&
+                         reinterpret_cast<uintptr_t>(c.x) % 16 == 0 &&
+                         (n_img - 1) * c.sx0 + (c.C - 1) * c.sx1 + (c.H - 1) * c.sx2 + c.W < (1ll << 31) &&
+                         (int64_t)xel < (1ll << 31);
+        if (vec)
+            tc::nchw_split_nhwc_vec_kernel<<<g, 256, 0, s>>>(c.x, (int)c.C, (int)c.H, (int)c.W, (int)Cp, (int)c.sx0,
+                                                             (int)c.sx1, (int)c.sx2, xhi, xlo, anyflag, gen);
+        else
+            tc::nchw_split_nhwc_kernel<<<g, 256, 0, s>>>(c.x, c.C, c.H, c.W, Cp, c.sx0, c.sx1, c.sx2, c.sx3, xhi,
+                                                         xlo, anyflag, gen);
         const int64_t wtot = co_tiles * tc::CN_BN * K;
         tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
             c.w, CO, K, K, c.C, Cp, c.S, c.sw0, c.sw1, c.sw2, c.sw3, wimg, anyflag, gen);

@@ -103,6 +103,43 @@ __global__ void __launch_bounds__(256) nchw_split_nhwc_kernel(const float *__res
     }
 }
 
+// Vectorised form (W % 4 == 0, unit w stride, sx1/sx2/sx0 multiples of 4,
+// 16-B aligned x, 32-bit indices): float4 reads along w, float4 writes along c
+__global__ void __launch_bounds__(256) nchw_split_nhwc_vec_kernel(const float *__restrict__ x, int C, int H, int W,
+                                                                  int Cp, int sx0, int sx1, int sx2,
+                                                                  float *__restrict__ hi, float *__restrict__ lo,
+                                                                  int *__restrict__ any, int gen) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    __shared__ float tile[32][33];   // [c][w]
+    const int nh = blockIdx.z;
+    const int n = nh / H, h = nh - n * H;
+    const int w0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const int t = threadIdx.x;
+    {
+        const int cc = t >> 3, w4 = (t & 7) * 4;
+        const int c = c0 + cc, w = w0 + w4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c < C && w < W) v = __ldg(reinterpret_cast<const float4 *>(x + n * sx0 + c * sx1 + h * sx2 + w));
+        tile[cc][w4] = v.x;
+        tile[cc][w4 + 1] = v.y;
+        tile[cc][w4 + 2] = v.z;
+        tile[cc][w4 + 3] = v.w;
+    }
+    __syncthreads();
+    const int ww = t >> 3, c4 = (t & 7) * 4;
+    const int w = w0 + ww, c = c0 + c4;
+    if (w < W && c < Cp) {
+        const float4 v = make_float4(tile[c4][ww], tile[c4 + 1][ww], tile[c4 + 2][ww], tile[c4 + 3][ww]);
+        const float4 vh = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+        const int64_t o = ((int64_t)nh * W + w) * Cp + c;
+        *reinterpret_cast<float4 *>(hi + o) = vh;
+        *reinterpret_cast<float4 *>(lo + o) =
+            make_float4(tf32_lo(v.x, vh.x), tf32_lo(v.y, vh.y), tf32_lo(v.z, vh.z), tf32_lo(v.w, vh.w));
+        const float inf = __int_as_float(0x7f800000);
+        if (!(fabsf(v.x) < inf && fabsf(v.y) < inf && fabsf(v.z) < inf && fabsf(v.w) < inf)) *any = gen;
+    }
+}
+
 // grid: x = image * tiles_h * tiles_w output tiles, y = channel tiles
 __global__ void __launch_bounds__(CN_THREADS, 2)
     tf32x3_conv_nhwc_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,

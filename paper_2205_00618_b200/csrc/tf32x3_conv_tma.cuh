@@ -107,31 +107,36 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 // taps in (r, s, c) order, so one 8 KiB bulk copy feeds a stage (a 2-D TMA
 // box of 64-B rows costs one request per row)
 // (tap k -> (r, s) = k / Cp, channel c = k % Cp; zero for c >= C or k >= K)
+// One thread per element with 32-bit index decomposition (the int64 div/mod
+// chain per element made this tiny prepass take 4.9 us on C3).
 __global__ void __launch_bounds__(256) filter_image_kernel(const float *__restrict__ w, int64_t CO, int64_t K,
                                                            int64_t Kp, int64_t C, int64_t Cp, int64_t S,
                                                            int64_t sw0, int64_t sw1, int64_t sw2, int64_t sw3,
                                                            float *__restrict__ img, int *__restrict__ any, int gen) {
     asm volatile("griddepcontrol.launch_dependents;");
-    const int64_t co_tiles = (CO + CT_BN - 1) / CT_BN, nkb = Kp / CT_BK;
-    const int64_t total = co_tiles * nkb * CT_BN * CT_BK;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int kk = (int)(e % CT_BK), n = (int)((e / CT_BK) % CT_BN);
-        const int64_t kb = (e / (CT_BK * CT_BN)) % nkb, ct = e / (CT_BK * CT_BN * nkb);
-        const int64_t co = ct * CT_BN + n, k = kb * CT_BK + kk;
+    const int nkb = (int)(Kp / CT_BK);
+    const int co_tiles = (int)((CO + CT_BN - 1) / CT_BN);
+    const int total = co_tiles * nkb * CT_BN * CT_BK;
+    const int cp = (int)Cp, sS = (int)S, kK = (int)K, cC = (int)C;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+        const int kk = e & (CT_BK - 1), n = (e >> 4) & (CT_BN - 1);
+        const int t = e >> 10;   // / (CT_BK * CT_BN)
+        const int kb = t % nkb, ct = t / nkb;
+        const int64_t co = (int64_t)ct * CT_BN + n;
+        const int k = kb * CT_BK + kk;
+        const int rs = k / cp, c = k - rs * cp;
         float v = 0.0f;
-        const int64_t rs = k / Cp, c = k % Cp;
-        if (co < CO && k < K && c < C) {
-            const int64_t r = rs / S, s = rs % S;
-            v = __ldg(w + co * sw0 + c * sw1 + r * sw2 + s * sw3);
+        if (co < CO && k < kK && c < cC) {
+            const int r = rs / sS, sx = rs - r * sS;
+            v = __ldg(w + co * sw0 + c * sw1 + r * sw2 + sx * sw3);
         }
         const float h = rna_tf32(v);
         const float l = tf32_lo(v, h);
         if (any != nullptr && !(fabsf(v) < __int_as_float(0x7f800000))) *any = gen;
-        const int64_t base = ((ct * nkb + kb) * 2) * (CT_BN * CT_BK);
+        float *base = img + ((int64_t)(ct * nkb + kb) * 2) * (CT_BN * CT_BK);
         const int off = n * 16 + (((kk >> 2) ^ ((n >> 1) & 3)) << 2) + (kk & 3);   // floats
-        img[base + off] = h;
-        img[base + CT_BN * CT_BK + off] = l;
+        base[off] = h;
+        base[CT_BN * CT_BK + off] = l;
     }
 }
 
