@@ -73,6 +73,38 @@ def test_small_case_forced_tensor_core_path(case, monkeypatch):
             assert common.strict_ok(got[slot], r).all(), case["name"]
 
 
+CONV_CASES = [c for c in SMALL if c["name"] in ("conv_valid_small", "conv_pad1_small", "conv_stride2_small",
+                                                 "acc_conv1d")]
+
+
+@pytest.mark.parametrize("algo", ["tf32x3_tma", "tf32x3_gather", "tf32x3_im2col", "simt"])
+@pytest.mark.parametrize("case", CONV_CASES, ids=[c["name"] for c in CONV_CASES])
+def test_conv_cases_every_conv_kernel(case, algo, monkeypatch):
+    """Each alternative conv kernel (TMA-fed converter kernel, in-kernel
+    gather, materialised im2col, SIMT) on the conv fixtures; kernels whose
+    preconditions fail fall back (lsb_conv2d_nchw) and must still be right."""
+    monkeypatch.setenv("LSB_GEMM_ALGO", algo)
+    gj = common.graph_json(case["graph"])
+    ins, ref, _ = common.case_data(case)
+    k, got = _run(gj, ins)
+    for slot, r in ref.items():
+        assert common.ref_metric(got[slot], r) <= 1e-4, case["name"]
+        if case["rule"] in ("tol", "exact"):
+            assert common.strict_ok(got[slot], r).all(), case["name"]
+
+
+@pytest.mark.parametrize("algo", ["tf32x3_tma", "tf32x3_gather"])
+def test_c3_alternative_conv_kernels(algo, monkeypatch):
+    monkeypatch.setenv("LSB_GEMM_ALGO", algo)
+    cfg = common.config("C3")
+    bufs = common.config_inputs("C3g")
+    k, got = _run(common.graph_json(cfg["graph_guarded"]), bufs)
+    o = got[2].reshape(8, 64, 56, 56)
+    d = np.load(common.GOLDEN + "/" + cfg["data"])
+    ref0 = d["ref_img0"].astype(np.float64).reshape(64, 56, 56)
+    assert common.strict_ok(o[0], ref0).all()
+
+
 def test_inputs_not_mutated_and_output_inserted():
     case = next(c for c in SMALL if c["name"] == "semiring_mul_add")
     ins, ref, _ = common.case_data(case)
