@@ -601,20 +601,22 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
             c.w, CO, K, K, c.C, Cp, c.S, c.sw0, c.sw1, c.sw2, c.sw3, wimg, anyflag, gen);
         if (aux_launches) *aux_launches = 2;
     }
-    CUtensorMap mh, ml;
+    CUtensorMap mxs;
     {
-        cuuint64_t dims[4] = {(cuuint64_t)Cp, (cuuint64_t)c.W, (cuuint64_t)c.H, (cuuint64_t)n_img};
-        cuuint64_t strides[3] = {(cuuint64_t)Cp * 4, (cuuint64_t)(c.W * Cp) * 4, (cuuint64_t)(c.H * c.W * Cp) * 4};
-        cuuint32_t box[4] = {(cuuint32_t)tc::CN_BK, (cuuint32_t)(32 * c.stride_w), (cuuint32_t)(4 * c.stride_h), 1};
-        cuuint32_t estr[4] = {1, (cuuint32_t)c.stride_w, (cuuint32_t)c.stride_h, 1};
-        for (int i = 0; i < 2; i++) {
-            CUresult r = g_encode(i ? &ml : &mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, i ? xlo : xhi, dims, strides, box,
-                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) {
-                snprintf(err, errlen, "cuTensorMapEncodeTiled failed (NHWC input, %d)", (int)r);
-                return LSB_ERR_CUDA;
-            }
+        // Xs[n][h][w][cb][32] as 5-D (32, cb, w, h, n); box = one channel block of
+        // 32 columns x 4 rows (every stride-th via element strides)
+        const int64_t cbn = Cp / 16;
+        cuuint64_t dims[5] = {32, (cuuint64_t)cbn, (cuuint64_t)c.W, (cuuint64_t)c.H, (cuuint64_t)n_img};
+        cuuint64_t strides[4] = {128, (cuuint64_t)cbn * 128, (cuuint64_t)(c.W * cbn) * 128,
+                                 (cuuint64_t)(c.H * c.W * cbn) * 128};
+        cuuint32_t box[5] = {32, 1, (cuuint32_t)(32 * c.stride_w), (cuuint32_t)(4 * c.stride_h), 1};
+        cuuint32_t estr[5] = {1, 1, (cuuint32_t)c.stride_w, (cuuint32_t)c.stride_h, 1};
+        CUresult r = g_encode(&mxs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, xhi, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            snprintf(err, errlen, "cuTensorMapEncodeTiled failed (NHWC input, %d)", (int)r);
+            return LSB_ERR_CUDA;
         }
     }
     static bool attr = false;
@@ -667,7 +669,7 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        cudaLaunchKernelEx(&cfg, tc::tf32x3_conv_nhwc_kernel, mh, ml, a);
+        cudaLaunchKernelEx(&cfg, tc::tf32x3_conv_nhwc_kernel, mxs, a);
     }
     prof_mark(1, s);
     if (trace_path) {

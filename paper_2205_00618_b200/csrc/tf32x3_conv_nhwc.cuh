@@ -2,10 +2,12 @@
 // an NHWC hi/lo copy of the input: implicit GEMM D[pixel][co] = Σ_(r,s,c)
 // X[pixel, tap] W[co, tap] in split-TF32 (Xhi.Whi + Xhi.Wlo + Xlo.Whi).
 //
-// Prepass (nchw_split_nhwc_kernel): X (any strides) -> Xhi, Xlo as [N][H][W][Cp]
-// (channels innermost, zero padded to Cp = 16k).  With channels innermost a
-// 16-channel x 32-column x 4-row box is exactly a K-major SWIZZLE_64B UMMA
-// operand (128 pixel rows of 64 B), and the tap's (r, s) shift lands on
+// Prepass (nchw_split_nhwc_kernel): X (any strides) -> Xs[N][H][W][Cp/16][32]:
+// per pixel and 16-channel block the 16 tf32 hi values then the 16 lo values
+// (channels zero padded to Cp = 16k).  With channels innermost a {32, 1 block,
+// 32 columns, 4 rows} box is exactly a K-major SWIZZLE_128B UMMA operand
+// (128 pixel rows of 128 B: hi at bytes 0-63, lo at 64-127; one TMA request
+// stream per stage instead of two 64-B-row boxes), and the tap's (r, s) shift lands on
 // non-innermost TMA coordinates, which may be any integer (out of range ->
 // zero fill = the conv padding; stride via TMA element strides).  So the
 // mainloop is the GEMM kernel's: no converter warps, no proxy fence, every
@@ -31,7 +33,7 @@ constexpr int CN_EPI_WARPS = 8;
 constexpr int CN_THREADS = 64 + 32 * CN_EPI_WARPS;   // 320
 constexpr int CN_CHUNKS = 2;
 constexpr int CN_ACC_COLS = 2 * CN_BN;
-constexpr int CN_TILE_A = 128 * CN_BK * 4;           // 8 KiB
+constexpr int CN_TILE_A = 128 * CN_BK * 4;           // 8 KiB (one of hi / lo)
 constexpr int CN_TILE_B = 2 * CN_BN * CN_BK * 4;     // 8 KiB (hi | lo)
 constexpr int CN_STAGE = 2 * CN_TILE_A + CN_TILE_B;  // 24 KiB
 constexpr size_t CN_SMEM = (size_t)CN_STAGES * CN_STAGE + 256 + 1024;
@@ -68,6 +70,15 @@ struct ConvNhwcArgs {
     } while (0)
 #endif
 
+__device__ __forceinline__ void tma_load_5d(const CUtensorMap *map, uint64_t *bar, void *dst, int c0, int c1, int c2,
+                                            int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+        : "memory");
+}
+
 // X[n][c][h][w] (element strides sx*) -> hi/lo [n][h][w][Cp], channels >= C
 // zero; 32 x 32 (w, c) tiles through smem so both sides are coalesced
 __global__ void __launch_bounds__(256) nchw_split_nhwc_kernel(const float *__restrict__ x, int64_t C, int64_t H,
@@ -95,9 +106,9 @@ __global__ void __launch_bounds__(256) nchw_split_nhwc_kernel(const float *__res
         if (w < W && c < Cp) {
             const float v = tile[tx][ww];
             const float vh = rna_tf32(v);
-            const int64_t o = ((nh * W) + w) * Cp + c;
+            const int64_t o = (((nh * W) + w) * (Cp / 16) + (c >> 4)) * 32 + (c & 15);
             hi[o] = vh;
-            lo[o] = tf32_lo(v, vh);
+            hi[o + 16] = tf32_lo(v, vh);
             if (!(fabsf(v) < __int_as_float(0x7f800000))) *any = gen;
         }
     }
@@ -131,9 +142,9 @@ __global__ void __launch_bounds__(256) nchw_split_nhwc_vec_kernel(const float *_
     if (w < W && c < Cp) {
         const float4 v = make_float4(tile[c4][ww], tile[c4 + 1][ww], tile[c4 + 2][ww], tile[c4 + 3][ww]);
         const float4 vh = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
-        const int64_t o = ((int64_t)nh * W + w) * Cp + c;
+        const int64_t o = (((int64_t)nh * W + w) * (Cp / 16) + (c >> 4)) * 32 + (c & 15);
         *reinterpret_cast<float4 *>(hi + o) = vh;
-        *reinterpret_cast<float4 *>(lo + o) =
+        *reinterpret_cast<float4 *>(hi + o + 16) =
             make_float4(tf32_lo(v.x, vh.x), tf32_lo(v.y, vh.y), tf32_lo(v.z, vh.z), tf32_lo(v.w, vh.w));
         const float inf = __int_as_float(0x7f800000);
         if (!(fabsf(v.x) < inf && fabsf(v.y) < inf && fabsf(v.z) < inf && fabsf(v.w) < inf)) *any = gen;
@@ -142,8 +153,7 @@ __global__ void __launch_bounds__(256) nchw_split_nhwc_vec_kernel(const float *_
 
 // grid: x = image * tiles_h * tiles_w output tiles, y = channel tiles
 __global__ void __launch_bounds__(CN_THREADS, 2)
-    tf32x3_conv_nhwc_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
-                            const ConvNhwcArgs p) {
+    tf32x3_conv_nhwc_kernel(const __grid_constant__ CUtensorMap map_xs, const ConvNhwcArgs p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + CN_STAGES * CN_STAGE);
@@ -168,8 +178,7 @@ __global__ void __launch_bounds__(CN_THREADS, 2)
 #endif
 
     if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&map_hi);
-        tma_prefetch_desc(&map_lo);
+        tma_prefetch_desc(&map_xs);
         for (int s = 0; s < CN_STAGES; s++) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -203,8 +212,7 @@ __global__ void __launch_bounds__(CN_THREADS, 2)
                 unsigned char *base = smem + stage * CN_STAGE;
                 mbar_expect_tx(&full[stage], CN_STAGE);
                 const int hi_ = hin0 + r * (int)p.dh, wi = win0 + s * (int)p.dw;
-                tma_load_4d(&map_hi, &full[stage], base, cb * CN_BK, wi, hi_, n);
-                tma_load_4d(&map_lo, &full[stage], base + CN_TILE_A, cb * CN_BK, wi, hi_, n);
+                tma_load_5d(&map_xs, &full[stage], base, 0, cb, wi, hi_, n);   // [pixel][hi16 | lo16]
                 bulk_load(base + 2 * CN_TILE_A, p.wimg + ((int64_t)blockIdx.y * num_kb + kb) * (2 * CN_BN * CN_BK),
                           CN_TILE_B, &full[stage]);
                 if (++cb == cblocks) {
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(CN_THREADS, 2)
                 const int chunk = kb / p.stages_per_chunk;
                 const uint32_t d = tmem + (uint32_t)(chunk * CN_ACC_COLS);
                 const uint32_t base = smem_u32(smem + stage * CN_STAGE);
-                const uint64_t ahi = sdesc_k_sw<64>(base), alo = sdesc_k_sw<64>(base + CN_TILE_A);
+                const uint64_t ahi = sdesc_k_sw<128>(base), alo = ahi + (uint64_t)(64 >> 4);   // lo: bytes 64-127
                 const uint64_t bhi = sdesc_k_sw<64>(base + 2 * CN_TILE_A);
 #pragma unroll
                 for (int k = 0; k < CN_BK / 8; k++) {
