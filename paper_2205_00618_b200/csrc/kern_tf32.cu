@@ -30,8 +30,10 @@ struct BKey {
     const float *B = nullptr;
     int64_t N = 0, K = 0, sb_k = 0, sb_n = 0, Kp = 0;
     const float *ws = nullptr;
+    int ilv = 0;
     bool operator==(const BKey &o) const {
-        return B == o.B && N == o.N && K == o.K && sb_k == o.sb_k && sb_n == o.sb_n && Kp == o.Kp && ws == o.ws;
+        return B == o.B && N == o.N && K == o.K && sb_k == o.sb_k && sb_n == o.sb_n && Kp == o.Kp && ws == o.ws &&
+               ilv == o.ilv;
     }
 };
 BKey g_bkey;
@@ -76,23 +78,24 @@ float *acquire_ws(size_t need, char *err, size_t errlen) {
 // split prepass of one operand viewed as X[r][k] = X[r*s_r + k*s_k] -> hi/lo
 // [R][Kp]: the vectorised kernels when the layout allows, else the scalar one
 void launch_split(const float *X, int64_t R, int64_t Kd, int64_t s_r, int64_t s_k, float *hi, float *lo, int64_t Kp,
-                  int *flag, int *any, int gen, cudaStream_t s) {
+                  int ilv, int *flag, int *any, int gen, cudaStream_t s) {
     const bool small = R * Kp < (1ll << 31) && R * std::max<int64_t>(s_r, 1) + Kd * std::max<int64_t>(s_k, 1) < (1ll << 31);
     const bool al = reinterpret_cast<uintptr_t>(X) % 16 == 0 && Kp % 4 == 0;
     if (small && al && s_k == 1 && s_r % 4 == 0 && Kd % 4 == 0 && !getenv("LSB_SCALAR_SPLIT")) {
         const int64_t units = R * (Kp / 4);
         const unsigned blocks = (unsigned)std::min<int64_t>((units + 255) / 256, 148 * 16);
-        tc::tf32_split_kcontig_kernel<<<blocks, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_r, hi, lo, (int)Kp, flag, any,
-                                                              gen);
+        tc::tf32_split_kcontig_kernel<<<blocks, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_r, hi, lo, (int)Kp, ilv, flag,
+                                                              any, gen);
         return;
     }
     if (small && al && s_r == 1 && s_k % 4 == 0 && R % 4 == 0 && !getenv("LSB_SCALAR_SPLIT")) {
         dim3 g((unsigned)((Kp + 31) / 32), (unsigned)((R + 31) / 32));
-        tc::tf32_split_rcontig_kernel<<<g, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_k, hi, lo, (int)Kp, flag, any, gen);
+        tc::tf32_split_rcontig_kernel<<<g, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_k, hi, lo, (int)Kp, ilv, flag, any,
+                                                              gen);
         return;
     }
     dim3 g((unsigned)((Kp + 31) / 32), (unsigned)((R + 31) / 32));
-    tc::tf32_split_kernel<<<g, 256, 0, s>>>(X, R, Kd, s_r, s_k, hi, lo, Kp, flag, any, gen);
+    tc::tf32_split_kernel<<<g, 256, 0, s>>>(X, R, Kd, s_r, s_k, hi, lo, Kp, ilv, flag, any, gen);
 }
 
 bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int bk, int box_rows) {
@@ -107,6 +110,19 @@ bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int 
     return r == CUDA_SUCCESS;
 }
 
+// interleaved split operand: rows of 2*Kp floats ([hi16 | lo16] per k block),
+// box = one k block (32 floats = 128 B) x box_rows, SWIZZLE_128B
+bool make_map_ilv(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int box_rows) {
+    cuuint64_t dims[2] = {(cuuint64_t)(2 * kp), (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(2 * kp) * sizeof(float)};
+    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // tensor maps + launch of the main kernel for one tile geometry; A rows are
 // output rows (m), B rows output columns (n), both K-major [rows][Kp]
 template <int BK, int BN>
@@ -114,8 +130,11 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
              int64_t n_rows, int64_t Kp, tc::TcArgs a, cudaStream_t s, char *err, size_t errlen) {
     using Cf = tc::Cfg<BK, BN>;
     CUtensorMap mah, mal, mbh, mbl;
-    if (!make_map(&mah, ahi, m_rows, Kp, BK, tc::BM) || !make_map(&mal, alo, m_rows, Kp, BK, tc::BM) ||
-        !make_map(&mbh, bhi, n_rows, Kp, BK, BN) || !make_map(&mbl, blo, n_rows, Kp, BK, BN)) {
+    const bool ok = a.ilv ? (make_map_ilv(&mah, ahi, m_rows, Kp, tc::BM) && make_map_ilv(&mbh, bhi, n_rows, Kp, BN) &&
+                             make_map_ilv(&mal, ahi, m_rows, Kp, tc::BM) && make_map_ilv(&mbl, bhi, n_rows, Kp, BN))
+                          : (make_map(&mah, ahi, m_rows, Kp, BK, tc::BM) && make_map(&mal, alo, m_rows, Kp, BK, tc::BM) &&
+                             make_map(&mbh, bhi, n_rows, Kp, BK, BN) && make_map(&mbl, blo, n_rows, Kp, BK, BN));
+    if (!ok) {
         snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
         return LSB_ERR_CUDA;
     }
@@ -208,6 +227,8 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     constexpr int kKAlign = 32;   // split buffers padded for either stage geometry
     const int64_t Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
     const size_t need = sizeof(float) * (size_t)(2 * M + 2 * N) * (size_t)Kp;
+    const int cfg = pick_cfg(N, K, epi.n > 0);
+    const int ilv = (cfg != 1 && !getenv("LSB_NO_ILV")) ? 1 : 0;   // BK = 16 tiles read [hi16 | lo16] rows
     float *ws;
     bool reuse_b = false;
     {
@@ -229,7 +250,7 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
         ws = g_split;
         // workspace layout [Bhi | Blo | Ahi | Alo]: B's split sits at a fixed
         // place, so row-block streaming of one contraction splits B once
-        const BKey key{B, N, K, sb_k, sb_n, Kp, ws};
+        const BKey key{B, N, K, sb_k, sb_n, Kp, ws, ilv};
         reuse_b = b_unchanged && key == g_bkey;
         g_bkey = key;
     }
@@ -264,8 +285,8 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
         bgen = g_bgen;
     }
     {
-        launch_split(A, M, K, sa_m, sa_k, ahi, alo, Kp, rowflag, anyflag, agen, s);
-        if (!reuse_b) launch_split(B, N, K, sb_n, sb_k, bhi, blo, Kp, colflag, anyflag + 1, bgen, s);
+        launch_split(A, M, K, sa_m, sa_k, ahi, alo, Kp, ilv, rowflag, anyflag, agen, s);
+        if (!reuse_b) launch_split(B, N, K, sb_n, sb_k, bhi, blo, Kp, ilv, colflag, anyflag + 1, bgen, s);
         if (aux_launches) *aux_launches = reuse_b ? 1 : 2;
     }
     tc::TcArgs a;
@@ -275,6 +296,7 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     a.epi = epi;
     a.rowflag = rowflag; a.colflag = colflag; a.anyflag = anyflag; a.done = done; a.agen = agen; a.bgen = bgen;
     a.ahi = ahi; a.alo = alo; a.bhi = bhi; a.blo = blo;
+    a.ilv = ilv;
     // fast epilogue when every stage is "(+ row-invariant operand[n]) then
     // identity|ReLU" with beta 1 and no C_in (C4's bias + ReLU)
     if (epi.n >= 1 && epi.n <= 2 && !getenv("LSB_NO_FAST_EPI")) {
@@ -295,7 +317,7 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
             a.frelu[0] = a.frelu[1] = 0;
         }
     }
-    return run_main_cfg(pick_cfg(N, K, epi.n > 0), ahi, alo, bhi, blo, M, N, Kp, a, s, err, errlen);
+    return run_main_cfg(cfg, ahi, alo, bhi, blo, M, N, Kp, a, s, err, errlen);
 }
 
 // NCHW conv on the tensor cores: im2col+split prepass of the input (B, one

@@ -85,6 +85,10 @@ struct TcArgs {
     // == bgen, written by the split prepass) are recomputed in FP32 from the
     // split operands (hi + lo == x exactly for non-finite x) -- IEEE results
     // like the reference's f64 evaluation; never taken for finite inputs
+    // ilv: split operands interleaved per 16-deep k block, rows of [hi16 | lo16]
+    // (2*Kp floats per row): one 128-B-row SWIZZLE_128B box per operand per
+    // stage instead of separate 64-B-row hi and lo boxes (BK = 16 tiles)
+    int ilv;
     const int *rowflag, *colflag, *anyflag;   // anyflag[0] A, [1] B
     int *done;                                 // CTA completion counter
     int agen, bgen;
@@ -229,7 +233,7 @@ __device__ __forceinline__ float tf32_lo(float x, float h) {
 // A row holding a non-finite value gets flag[r] = gen (see TcArgs::rowflag).
 __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict__ X, int64_t R, int64_t Kd,
                                                          int64_t s_r, int64_t s_k, float *__restrict__ hi,
-                                                         float *__restrict__ lo, int64_t Kp,
+                                                         float *__restrict__ lo, int64_t Kp, int ilv,
                                                          int *__restrict__ flag, int *__restrict__ any, int gen) {
     __shared__ float tile[32][33];
     const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
@@ -251,8 +255,9 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
         if (r < R && k < Kp) {
             float x = tile[a][tx];
             float h = rna_tf32(x);
-            hi[r * Kp + k] = h;
-            lo[r * Kp + k] = tf32_lo(x, h);
+            const int64_t o = ilv ? r * 2 * Kp + (k >> 4) * 32 + (k & 15) : r * Kp + k;
+            hi[o] = h;
+            (ilv ? hi + 16 : lo)[o] = tf32_lo(x, h);
             if (flag != nullptr && !(fabsf(x) < __int_as_float(0x7f800000))) {
                 flag[r] = gen;
                 *any = gen;
@@ -270,9 +275,14 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
 //    float4 reads along r and float4 writes along k
 // Preconditions (checked by the host): 16-B aligned X, the contiguous extent
 // and the other stride multiples of 4, every index < 2^31.
+// (ilv: hi/lo land interleaved in `hi` per 16-k block, see TcArgs::ilv)
+__device__ __forceinline__ int64_t split_off(int64_t r, int64_t k, int64_t Kp, int ilv) {
+    return ilv ? r * 2 * Kp + (k >> 4) * 32 + (k & 15) : r * Kp + k;
+}
+
 __global__ void __launch_bounds__(256) tf32_split_kcontig_kernel(const float *__restrict__ X, int R, int Kd, int s_r,
                                                                  float *__restrict__ hi, float *__restrict__ lo,
-                                                                 int Kp, int *__restrict__ flag,
+                                                                 int Kp, int ilv, int *__restrict__ flag,
                                                                  int *__restrict__ any, int gen) {
     asm volatile("griddepcontrol.launch_dependents;");
     const int q4 = Kp / 4;
@@ -283,9 +293,9 @@ __global__ void __launch_bounds__(256) tf32_split_kcontig_kernel(const float *__
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (k < Kd) v = __ldg(reinterpret_cast<const float4 *>(X + (int64_t)r * s_r + k));
         const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
-        const int64_t o = (int64_t)r * Kp + k;
+        const int64_t o = split_off(r, k, Kp, ilv);
         *reinterpret_cast<float4 *>(hi + o) = h;
-        *reinterpret_cast<float4 *>(lo + o) =
+        *reinterpret_cast<float4 *>((ilv ? hi + 16 : lo) + o) =
             make_float4(tf32_lo(v.x, h.x), tf32_lo(v.y, h.y), tf32_lo(v.z, h.z), tf32_lo(v.w, h.w));
         if (flag != nullptr && !(fabsf(v.x) < inf && fabsf(v.y) < inf && fabsf(v.z) < inf && fabsf(v.w) < inf)) {
             flag[r] = gen;
@@ -296,7 +306,7 @@ __global__ void __launch_bounds__(256) tf32_split_kcontig_kernel(const float *__
 
 __global__ void __launch_bounds__(256) tf32_split_rcontig_kernel(const float *__restrict__ X, int R, int Kd, int s_k,
                                                                  float *__restrict__ hi, float *__restrict__ lo,
-                                                                 int Kp, int *__restrict__ flag,
+                                                                 int Kp, int ilv, int *__restrict__ flag,
                                                                  int *__restrict__ any, int gen) {
     asm volatile("griddepcontrol.launch_dependents;");
     __shared__ float tile[32][33];   // [k][r]
@@ -318,9 +328,9 @@ __global__ void __launch_bounds__(256) tf32_split_rcontig_kernel(const float *__
     if (r < R && k < Kp) {
         const float4 v = make_float4(tile[k4][rr], tile[k4 + 1][rr], tile[k4 + 2][rr], tile[k4 + 3][rr]);
         const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
-        const int64_t o = (int64_t)r * Kp + k;
+        const int64_t o = split_off(r, k, Kp, ilv);
         *reinterpret_cast<float4 *>(hi + o) = h;
-        *reinterpret_cast<float4 *>(lo + o) =
+        *reinterpret_cast<float4 *>((ilv ? hi + 16 : lo) + o) =
             make_float4(tf32_lo(v.x, h.x), tf32_lo(v.y, h.y), tf32_lo(v.z, h.z), tf32_lo(v.w, h.w));
         const float inf = __int_as_float(0x7f800000);
         if (flag != nullptr && !(fabsf(v.x) < inf && fabsf(v.y) < inf && fabsf(v.z) < inf && fabsf(v.w) < inf)) {
@@ -438,9 +448,18 @@ __device__ void tc_nonfinite_fixup(const TcArgs &p) {
     if (!s_last) return;
     __threadfence();
     auto fix = [&](int64_t m, int64_t n) {
-        const float *ah = p.ahi + m * p.Kp, *al = p.alo + m * p.Kp, *bh = p.bhi + n * p.Kp, *bl = p.blo + n * p.Kp;
         float acc = 0.0f;
-        for (int64_t k = 0; k < p.K; k++) acc = fmaf(ah[k] + al[k], bh[k] + bl[k], acc);
+        if (p.ilv) {
+            const float *a = p.ahi + m * 2 * p.Kp, *b = p.bhi + n * 2 * p.Kp;
+            for (int64_t k = 0; k < p.K; k++) {
+                const int64_t o = (k >> 4) * 32 + (k & 15);
+                acc = fmaf(a[o] + a[o + 16], b[o] + b[o + 16], acc);
+            }
+        } else {
+            const float *ah = p.ahi + m * p.Kp, *al = p.alo + m * p.Kp, *bh = p.bhi + n * p.Kp,
+                        *bl = p.blo + n * p.Kp;
+            for (int64_t k = 0; k < p.K; k++) acc = fmaf(ah[k] + al[k], bh[k] + bl[k], acc);
+        }
         if (p.epi.n) acc = apply_epilogue(p.epi, acc, 0, m, n, 0);
         p.C[m * p.sc_m + n * p.sc_n] = acc;
     };
@@ -533,10 +552,15 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 unsigned char *base = smem + stage * kStageBytes;
                 mbar_expect_tx(&full[stage], kStageBytes);
                 const int kx = kb * BK;
-                tma_load_2d(&map_ahi, &full[stage], base, kx, (int)m0);
-                tma_load_2d(&map_alo, &full[stage], base + kTileA, kx, (int)m0);
-                tma_load_2d(&map_bhi, &full[stage], base + 2 * kTileA, kx, (int)n0);
-                tma_load_2d(&map_blo, &full[stage], base + 2 * kTileA + kTileB, kx, (int)n0);
+                if (p.ilv) {   // [A rows: hi16 | lo16][B rows: hi16 | lo16]
+                    tma_load_2d(&map_ahi, &full[stage], base, 2 * kx, (int)m0);
+                    tma_load_2d(&map_bhi, &full[stage], base + 2 * kTileA, 2 * kx, (int)n0);
+                } else {
+                    tma_load_2d(&map_ahi, &full[stage], base, kx, (int)m0);
+                    tma_load_2d(&map_alo, &full[stage], base + kTileA, kx, (int)m0);
+                    tma_load_2d(&map_bhi, &full[stage], base + 2 * kTileA, kx, (int)n0);
+                    tma_load_2d(&map_blo, &full[stage], base + 2 * kTileA + kTileB, kx, (int)n0);
+                }
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -562,10 +586,18 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                     TC_TRACE(0, kb);
                     tc_fence_after();
                     const uint32_t base = smem_u32(smem + stage * kStageBytes);
-                    const uint64_t ahi = sdesc_k_sw<Cf::kSwizzleBytes>(base);
-                    const uint64_t alo = sdesc_k_sw<Cf::kSwizzleBytes>(base + kTileA);
-                    const uint64_t bhi = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileA);
-                    const uint64_t blo = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileA + kTileB);
+                    uint64_t ahi, alo, bhi, blo;
+                    if (p.ilv) {   // lo = the second 64 B of each 128-B row
+                        ahi = sdesc_k_sw<128>(base);
+                        alo = ahi + (uint64_t)(64 >> 4);
+                        bhi = sdesc_k_sw<128>(base + 2 * kTileA);
+                        blo = bhi + (uint64_t)(64 >> 4);
+                    } else {
+                        ahi = sdesc_k_sw<Cf::kSwizzleBytes>(base);
+                        alo = sdesc_k_sw<Cf::kSwizzleBytes>(base + kTileA);
+                        bhi = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileA);
+                        blo = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileA + kTileB);
+                    }
 #pragma unroll
                     for (int k = 0; k < BK / 8; k++) {
                         const uint64_t off = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along K
