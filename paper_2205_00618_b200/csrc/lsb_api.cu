@@ -363,8 +363,11 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     GemmFn fn = nullptr;
     int bm = 128;
     if (!d->beta_in_loop) {
-        // 64-row tiles only when the rows would leave half a 128-row tile idle
-        bm = (d->tile_m == 64 || (d->tile_m == 0 && M <= 64)) ? 64 : 128;
+        // 64-row tiles when the rows would leave half a 128-row tile idle, and
+        // for tiny problems (C1 256^3: latency-bound, more and shorter CTAs win;
+        // tools/small_gemm_sweep.py: 20.4 -> 14.2 us with 64-row tiles + 16 splits)
+        const bool tiny = (double)M * d->N * d->K * d->batch <= (double)(1 << 26);
+        bm = (d->tile_m == 64 || (d->tile_m == 0 && (M <= 64 || tiny))) ? 64 : 128;
         // two-level accumulation for long fp32 sums (K split into 256-chunks)
         const bool two = d->reduce == LSB_OP_ADD && d->K > 1024;
         fn = fast_gemm(d->combine, d->reduce, bm, two);
@@ -414,6 +417,10 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
                 const double cost = (double)waves / s + 0.05 * s;
                 if (cost < best - 1e-9) { best = cost; splits = s; }
             }
+            // tiny problems are latency-bound: as many splits as fit one wave
+            // (>= 2 k-slices each), the fold is cheap at this size
+            if ((double)M * d->N * d->K * d->batch <= (double)(1 << 26))
+                splits = (int)std::max<int64_t>(1, std::min<int64_t>({16, k_slices / 2, slots / std::max<int64_t>(1, tiles)}));
         }
     }
     int64_t kps = (d->K + splits - 1) / splits;
