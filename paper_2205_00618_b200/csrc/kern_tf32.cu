@@ -499,8 +499,10 @@ int tf32x3_conv_tma(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_l
     if (!ws) return LSB_ERR_NOMEM;
     const int64_t co_tiles = (CO + tc::CT_BN - 1) / tc::CT_BN;
     const int64_t wtot = co_tiles * Kp * tc::CT_BN;
-    tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
-        c.w, CO, K, Kp, c.C, c.C, c.S, c.sw0, c.sw1, c.sw2, c.sw3, ws, nullptr, 0);
+    {
+        tc::FilterImgArgs f{c.w, CO, K, Kp, c.C, c.C, c.S, {c.sw0, c.sw1, c.sw2, c.sw3}, ws};
+        tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(f, nullptr, 0);
+    }
     if (aux_launches) *aux_launches = 1;
     CUtensorMap mx;
     {
@@ -612,16 +614,25 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
                          reinterpret_cast<uintptr_t>(c.x) % 16 == 0 &&
                          (n_img - 1) * c.sx0 + (c.C - 1) * c.sx1 + (c.H - 1) * c.sx2 + c.W < (1ll << 31) &&
                          (int64_t)xel < (1ll << 31);
-        if (vec)
-            tc::nchw_split_nhwc_vec_kernel<<<g, 256, 0, s>>>(c.x, (int)c.C, (int)c.H, (int)c.W, (int)Cp, (int)c.sx0,
-                                                             (int)c.sx1, (int)c.sx2, xhi, xlo, anyflag, gen);
-        else
+        const int64_t wtot = co_tiles * tc::CN_BN * K;
+        tc::FilterImgArgs f{c.w, CO, K, K, c.C, Cp, c.S, {c.sw0, c.sw1, c.sw2, c.sw3}, wimg};
+        if (vec) {
+            // one launch: X split blocks, then ceil(filter blocks / (gx*gy)) z-slices of filter work
+            const unsigned zsplit = (unsigned)(n_img * ((c.H + tc::kSplitRows - 1) / tc::kSplitRows));
+            const int64_t fblocks = std::min<int64_t>((wtot + 255) / 256, 4096);
+            const unsigned zf = (unsigned)((fblocks + g.x * g.y - 1) / (g.x * g.y));
+            const dim3 gv(g.x, g.y, zsplit + zf);
+            tc::nchw_split_nhwc_vec_kernel<<<gv, 256, 0, s>>>(c.x, (int)c.C, (int)c.H, (int)c.W, (int)Cp, (int)c.sx0,
+                                                              (int)c.sx1, (int)c.sx2, xhi, xlo, anyflag, gen, f,
+                                                              (int)zsplit);
+            if (aux_launches) *aux_launches = 1;
+        } else {
             tc::nchw_split_nhwc_kernel<<<g, 256, 0, s>>>(c.x, c.C, c.H, c.W, Cp, c.sx0, c.sx1, c.sx2, c.sx3, xhi,
                                                          xlo, anyflag, gen);
-        const int64_t wtot = co_tiles * tc::CN_BN * K;
-        tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
-            c.w, CO, K, K, c.C, Cp, c.S, c.sw0, c.sw1, c.sw2, c.sw3, wimg, anyflag, gen);
-        if (aux_launches) *aux_launches = 2;
+            tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
+                f, anyflag, gen);
+            if (aux_launches) *aux_launches = 2;
+        }
     }
     CUtensorMap mxs;
     {

@@ -391,7 +391,8 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
             !d->beta_in_loop && d->beta == 1.0f && a.epi.n == 0 && d->batch == 1 && d->split_k == 0 &&
             t128 < 3 * slots && d->K >= 64 * lsb::kBK && !getenv("LSB_NO_STREAMK")) {
             const int64_t units = t128 * ((d->K + lsb::kBK - 1) / lsb::kBK);
-            const int ctas = (int)std::min<int64_t>(slots, std::max<int64_t>(1, units / 16));
+            int ctas = (int)std::min<int64_t>(slots, std::max<int64_t>(1, units / 16));
+            if (const char *e = getenv("LSB_STREAMK_CTAS")) ctas = std::max(1, atoi(e));
             lsb::prof_mark(0, s);
             lsb::launch_streamk(d->reduce, a, ctas, s);
             lsb::prof_mark(1, s);

@@ -116,39 +116,67 @@ __global__ void __launch_bounds__(256) nchw_split_nhwc_kernel(const float *__res
 
 // Vectorised form (W % 4 == 0, unit w stride, sx1/sx2/sx0 multiples of 4,
 // 16-B aligned x, 32-bit indices): float4 reads along w, float4 writes along c
+// kRows input rows per block: their kRows float4 loads are in flight
+// together (one row per block left the transpose latency-bound at ~2x the
+// copy time)
+constexpr int kSplitRows = 4;
+// Blocks with blockIdx.z >= zsplit build the filter stage images instead
+// (one launch for both prepasses; they run side by side).
 __global__ void __launch_bounds__(256) nchw_split_nhwc_vec_kernel(const float *__restrict__ x, int C, int H, int W,
                                                                   int Cp, int sx0, int sx1, int sx2,
                                                                   float *__restrict__ hi, float *__restrict__ lo,
-                                                                  int *__restrict__ any, int gen) {
+                                                                  int *__restrict__ any, int gen,
+                                                                  const FilterImgArgs f, int zsplit) {
     asm volatile("griddepcontrol.launch_dependents;");
-    __shared__ float tile[32][33];   // [c][w]
-    const int nh = blockIdx.z;
-    const int n = nh / H, h = nh - n * H;
+    if ((int)blockIdx.z >= zsplit) {
+        const int b = ((blockIdx.z - zsplit) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        const int nb = (gridDim.z - zsplit) * gridDim.y * gridDim.x;
+        filter_image_body(f, any, gen, b * blockDim.x + threadIdx.x, nb * blockDim.x);
+        return;
+    }
+    __shared__ float tile[kSplitRows][32][33];   // [row][c][w]
+    const int hblocks = (H + kSplitRows - 1) / kSplitRows;
+    const int n = blockIdx.z / hblocks, hb = (blockIdx.z - n * hblocks) * kSplitRows;
     const int w0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     const int t = threadIdx.x;
     {
         const int cc = t >> 3, w4 = (t & 7) * 4;
         const int c = c0 + cc, w = w0 + w4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (c < C && w < W) v = __ldg(reinterpret_cast<const float4 *>(x + n * sx0 + c * sx1 + h * sx2 + w));
-        tile[cc][w4] = v.x;
-        tile[cc][w4 + 1] = v.y;
-        tile[cc][w4 + 2] = v.z;
-        tile[cc][w4 + 3] = v.w;
+        float4 v[kSplitRows];
+#pragma unroll
+        for (int q = 0; q < kSplitRows; q++) {
+            v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c < C && w < W && hb + q < H)
+                v[q] = __ldg(reinterpret_cast<const float4 *>(x + n * sx0 + c * sx1 + (hb + q) * sx2 + w));
+        }
+#pragma unroll
+        for (int q = 0; q < kSplitRows; q++) {
+            tile[q][cc][w4] = v[q].x;
+            tile[q][cc][w4 + 1] = v[q].y;
+            tile[q][cc][w4 + 2] = v[q].z;
+            tile[q][cc][w4 + 3] = v[q].w;
+        }
     }
     __syncthreads();
     const int ww = t >> 3, c4 = (t & 7) * 4;
     const int w = w0 + ww, c = c0 + c4;
-    if (w < W && c < Cp) {
-        const float4 v = make_float4(tile[c4][ww], tile[c4 + 1][ww], tile[c4 + 2][ww], tile[c4 + 3][ww]);
-        const float4 vh = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
-        const int64_t o = (((int64_t)nh * W + w) * (Cp / 16) + (c >> 4)) * 32 + (c & 15);
-        *reinterpret_cast<float4 *>(hi + o) = vh;
-        *reinterpret_cast<float4 *>(hi + o + 16) =
-            make_float4(tf32_lo(v.x, vh.x), tf32_lo(v.y, vh.y), tf32_lo(v.z, vh.z), tf32_lo(v.w, vh.w));
-        const float inf = __int_as_float(0x7f800000);
-        if (!(fabsf(v.x) < inf && fabsf(v.y) < inf && fabsf(v.z) < inf && fabsf(v.w) < inf)) *any = gen;
+    const float inf = __int_as_float(0x7f800000);
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < kSplitRows; q++) {
+        if (w < W && c < Cp && hb + q < H) {
+            const float4 v =
+                make_float4(tile[q][c4][ww], tile[q][c4 + 1][ww], tile[q][c4 + 2][ww], tile[q][c4 + 3][ww]);
+            const float4 vh = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+            const int64_t nh = (int64_t)n * H + hb + q;
+            const int64_t o = ((nh * W + w) * (Cp / 16) + (c >> 4)) * 32 + (c & 15);
+            *reinterpret_cast<float4 *>(hi + o) = vh;
+            *reinterpret_cast<float4 *>(hi + o + 16) =
+                make_float4(tf32_lo(v.x, vh.x), tf32_lo(v.y, vh.y), tf32_lo(v.z, vh.z), tf32_lo(v.w, vh.w));
+            bad |= !(fabsf(v.x) < inf && fabsf(v.y) < inf && fabsf(v.z) < inf && fabsf(v.w) < inf);
+        }
     }
+    if (bad) *any = gen;
 }
 
 // grid: x = image * tiles_h * tiles_w output tiles, y = channel tiles

@@ -108,17 +108,21 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 // box of 64-B rows costs one request per row)
 // (tap k -> (r, s) = k / Cp, channel c = k % Cp; zero for c >= C or k >= K)
 // One thread per element with 32-bit index decomposition (the int64 div/mod
-// chain per element made this tiny prepass take 4.9 us on C3).
-__global__ void __launch_bounds__(256) filter_image_kernel(const float *__restrict__ w, int64_t CO, int64_t K,
-                                                           int64_t Kp, int64_t C, int64_t Cp, int64_t S,
-                                                           int64_t sw0, int64_t sw1, int64_t sw2, int64_t sw3,
-                                                           float *__restrict__ img, int *__restrict__ any, int gen) {
-    asm volatile("griddepcontrol.launch_dependents;");
-    const int nkb = (int)(Kp / CT_BK);
-    const int co_tiles = (int)((CO + CT_BN - 1) / CT_BN);
+// chain per element made this tiny prepass take 4.9 us on C3).  The body is
+// shared with the NHWC conv's fused prepass (extra blocks of its X split).
+struct FilterImgArgs {
+    const float *w;
+    int64_t CO, K, Kp, C, Cp, S;
+    int64_t sw[4];
+    float *img;
+};
+
+__device__ __forceinline__ void filter_image_body(const FilterImgArgs &f, int *any, int gen, int first, int step) {
+    const int nkb = (int)(f.Kp / CT_BK);
+    const int co_tiles = (int)((f.CO + CT_BN - 1) / CT_BN);
     const int total = co_tiles * nkb * CT_BN * CT_BK;
-    const int cp = (int)Cp, sS = (int)S, kK = (int)K, cC = (int)C;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int cp = (int)f.Cp, sS = (int)f.S, kK = (int)f.K, cC = (int)f.C;
+    for (int e = first; e < total; e += step) {
         const int kk = e & (CT_BK - 1), n = (e >> 4) & (CT_BN - 1);
         const int t = e >> 10;   // / (CT_BK * CT_BN)
         const int kb = t % nkb, ct = t / nkb;
@@ -126,18 +130,23 @@ __global__ void __launch_bounds__(256) filter_image_kernel(const float *__restri
         const int k = kb * CT_BK + kk;
         const int rs = k / cp, c = k - rs * cp;
         float v = 0.0f;
-        if (co < CO && k < kK && c < cC) {
+        if (co < f.CO && k < kK && c < cC) {
             const int r = rs / sS, sx = rs - r * sS;
-            v = __ldg(w + co * sw0 + c * sw1 + r * sw2 + sx * sw3);
+            v = __ldg(f.w + co * f.sw[0] + c * f.sw[1] + r * f.sw[2] + sx * f.sw[3]);
         }
         const float h = rna_tf32(v);
         const float l = tf32_lo(v, h);
         if (any != nullptr && !(fabsf(v) < __int_as_float(0x7f800000))) *any = gen;
-        float *base = img + ((int64_t)(ct * nkb + kb) * 2) * (CT_BN * CT_BK);
+        float *base = f.img + ((int64_t)(ct * nkb + kb) * 2) * (CT_BN * CT_BK);
         const int off = n * 16 + (((kk >> 2) ^ ((n >> 1) & 3)) << 2) + (kk & 3);   // floats
         base[off] = h;
         base[CT_BN * CT_BK + off] = l;
     }
+}
+
+__global__ void __launch_bounds__(256) filter_image_kernel(const FilterImgArgs f, int *__restrict__ any, int gen) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    filter_image_body(f, any, gen, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 __device__ __forceinline__ void split4_store(uint32_t dst_hi, uint32_t dst_lo, float a, float b, float c, float d) {
