@@ -75,6 +75,84 @@ __global__ void probe(const float *A, const float *B, float *D, uint32_t lbo, ui
     if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
 }
 
+// conv-pattern stage: for k in 0..1: N=128 (A hi, SW128 K-major) + N=64 (A lo at +64 B);
+// B K-major SW64 (128 rows).  mode 0: that; mode 1: A SW64 (separate hi/lo tiles);
+// mode 2: three N=64 MMAs per k (the old pattern); mode 3: N=256 x 2 per k (GEMM-like)
+__global__ void conv_pattern(int mode, int n_iter, long long *out) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + 65536);
+    uint32_t *slot = reinterpret_cast<uint32_t *>(smem + 65600);
+    int t = threadIdx.x;
+    for (int e = t; e < 16384; e += blockDim.x) reinterpret_cast<float *>(smem)[e] = 0.5f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (t == 0) { mbar_init(bar, 1); mbar_init(bar + 2, 1 << 20); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    if (t < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    uint32_t tmem = *slot;
+    if (t == 0) {
+        const uint32_t base = smem_u32(smem);
+        const uint32_t i64 = idesc_tf32(128, 64), i128 = idesc_tf32(128, 128), i256 = idesc_tf32(128, 256);
+        long long t0 = clock64();
+        for (int it = 0; it < n_iter; it++) {
+            if (mode >= 6) {   // mode 6/7/8: M=64 N=256 / M=64 N=128 / M=128 N=256, 2 per k
+                const uint64_t a = sdesc_k_sw<64>(base), b = sdesc_k_sw<64>(base + 32768);
+                const uint32_t id = mode == 6 ? idesc_tf32(64, 256) : mode == 7 ? idesc_tf32(64, 128) : idesc_tf32(128, 256);
+                for (int k = 0; k < 2; k++) {
+                    const uint64_t off = (uint64_t)((k * 32) >> 4);
+                    umma_tf32(tmem, a + off, b + off, id, 1u);
+                    umma_tf32(tmem, a + off, b + off, id, 1u);
+                }
+                continue;
+            }
+            if (mode >= 4) {   // mode 4: conv stage + commit every stage; 5: every 4th stage
+                const uint64_t a = sdesc_k_sw<128>(base), b = sdesc_k_sw<64>(base + 32768);
+                for (int k = 0; k < 2; k++) {
+                    const uint64_t off = (uint64_t)((k * 32) >> 4);
+                    umma_tf32(tmem, a + off, b + off, i128, 1u);
+                    umma_tf32(tmem, a + 4 + off, b + off, i64, 1u);
+                }
+                if (mode == 4 || (it & 3) == 3) umma_commit(bar + 2);
+                continue;
+            }
+            for (int k = 0; k < 2; k++) {
+                const uint64_t off = (uint64_t)((k * 32) >> 4);
+                if (mode == 0) {
+                    const uint64_t a = sdesc_k_sw<128>(base), b = sdesc_k_sw<64>(base + 32768);
+                    umma_tf32(tmem, a + off, b + off, i128, 1u);
+                    umma_tf32(tmem, a + 4 + off, b + off, i64, 1u);
+                } else if (mode == 1) {
+                    const uint64_t a = sdesc_k_sw<64>(base), al = sdesc_k_sw<64>(base + 8192), b = sdesc_k_sw<64>(base + 32768);
+                    umma_tf32(tmem, a + off, b + off, i128, 1u);
+                    umma_tf32(tmem, al + off, b + off, i64, 1u);
+                } else if (mode == 2) {
+                    const uint64_t a = sdesc_k_sw<64>(base), al = sdesc_k_sw<64>(base + 8192), b = sdesc_k_sw<64>(base + 32768), bl = sdesc_k_sw<64>(base + 36864);
+                    umma_tf32(tmem, a + off, b + off, i64, 1u);
+                    umma_tf32(tmem, a + off, bl + off, i64, 1u);
+                    umma_tf32(tmem, al + off, b + off, i64, 1u);
+                } else {
+                    const uint64_t a = sdesc_k_sw<64>(base), al = sdesc_k_sw<64>(base + 8192), b = sdesc_k_sw<64>(base + 32768);
+                    umma_tf32(tmem, a + off, b + off, i256, 1u);
+                    umma_tf32(tmem, a + off, b + off, i256, 1u);
+                    umma_tf32(tmem, al + off, b + off, i256, 1u);
+                }
+            }
+        }
+        umma_commit(bar);
+        mbar_wait(bar, 0);
+        long long t1 = clock64();
+        out[0] = t1 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
 __global__ void mma_lat(int kmajor_a, int n_iter, int per, long long *out, int nn) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -83,7 +161,7 @@ __global__ void mma_lat(int kmajor_a, int n_iter, int per, long long *out, int n
     int t = threadIdx.x;
     for (int e = t; e < 8192; e += blockDim.x) reinterpret_cast<float *>(smem)[e] = 0.5f;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (t == 0) { mbar_init(bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    if (t == 0) { mbar_init(bar, 1); mbar_init(bar + 2, 1 << 20); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
     if (t < 32) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(256));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -120,6 +198,17 @@ __global__ void mma_lat(int kmajor_a, int n_iter, int per, long long *out, int n
 }
 
 int main() {
+    {
+        long long *o2, hh;
+        cudaMalloc(&o2, 8);
+        cudaFuncSetAttribute(conv_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+        for (int mode = 0; mode < 9; mode++) {
+            conv_pattern<<<1, 128, 70000>>>(mode, 200, o2);
+            cudaError_t e = cudaDeviceSynchronize();
+            cudaMemcpy(&hh, o2, 8, cudaMemcpyDeviceToHost);
+            printf("conv pattern mode %d %s: %.1f cycles per 16-tap stage\n", mode, cudaGetErrorString(e), hh / 200.0);
+        }
+    }
     {
         long long *o, h[2];
         cudaMalloc(&o, 16);
