@@ -684,6 +684,41 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 if (n < p.N) epi4_preload(p.epi, n, n + 3 < p.N, pre[h]);
             }
         }
+        if (p.fast_n && p.conv_hw == 0 && p.c_vec) {
+            // fast epilogue, its own loop: bias adds and ReLUs only, no
+            // per-element dispatch on the generic stage table
+            const bool b0 = p.fbias[0] != nullptr, r0 = p.frelu[0] != 0;
+            const bool b1 = p.fast_n > 1 && p.fbias[1] != nullptr, r1 = p.fast_n > 1 && p.frelu[1] != 0;
+#pragma unroll 2
+            for (int rr = 0; rr < kRowsPerWarp; rr++) {
+                const int r = ew * kRowsPerWarp + rr;
+                const int64_t m = m0 + r;
+                if (m >= p.M) continue;
+                float *dst = p.C + m * p.sc_m;
+#pragma unroll
+                for (int h = 0; h < BN / 128; h++) {
+                    const int chunk = h * 32 + lane;
+                    const int pos = chunk ^ (r & 31);
+                    const float4 v = *reinterpret_cast<const float4 *>(tile + r * BN + pos * 4);
+                    const int64_t n = n0 + chunk * 4;
+                    float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        if (b0) x[e] += fpre[h][0][e];
+                        if (r0) x[e] = fmax_nan(x[e], 0.0f);
+                        if (b1) x[e] += fpre[h][1][e];
+                        if (r1) x[e] = fmax_nan(x[e], 0.0f);
+                    }
+                    if (n + 3 < p.N) {
+                        *reinterpret_cast<float4 *>(dst + n) = make_float4(x[0], x[1], x[2], x[3]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; e++)
+                            if (n + e < p.N) dst[n + e] = x[e];
+                    }
+                }
+            }
+        } else
 #pragma unroll 1
         for (int rr = 0; rr < kRowsPerWarp; rr++) {
             const int r = ew * kRowsPerWarp + rr;
@@ -717,7 +752,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
 #pragma unroll
                         for (int e = 0; e < 4; e++) {
                             if (p.fbias[i]) x[e] += fpre[h][i][e];
-                            if (p.frelu[i]) x[e] = fmaxf(x[e], 0.0f);
+                            if (p.frelu[i]) x[e] = fmax_nan(x[e], 0.0f);
                         }
                     }
                 } else if (p.epi.n) {
