@@ -684,9 +684,9 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 if (n < p.N) epi4_preload(p.epi, n, n + 3 < p.N, pre[h]);
             }
         }
-        if (p.fast_n && p.conv_hw == 0 && p.c_vec) {
-            // fast epilogue, its own loop: bias adds and ReLUs only, no
-            // per-element dispatch on the generic stage table
+        if ((p.fast_n || p.epi.n == 0) && p.conv_hw == 0 && p.c_vec) {
+            // no epilogue or the fast one, in its own loop: bias adds and ReLUs
+            // only, no per-element dispatch on the generic stage table
             const bool b0 = p.fbias[0] != nullptr, r0 = p.frelu[0] != 0;
             const bool b1 = p.fast_n > 1 && p.fbias[1] != nullptr, r1 = p.fast_n > 1 && p.frelu[1] != 0;
 #pragma unroll 2
