@@ -342,12 +342,17 @@ def roofline(steps, achieved, fp32_peak, sm_max, info, clocks, pk) -> dict:
                  "(MEASURED_PEAKS sm_max_mhz; no measured FP32 SIMT figure exists)")
     if any("tf32x3" in s for s in steps) and pk.get("bf16_tflops_sustained"):
         peak = pk["bf16_tflops_sustained"] / 2.0 / 3.0
-        return {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 2),
+        out = {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 2),
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
                 "peak_source": "measured bf16 sustained (MEASURED_PEAKS) / 2 (tf32) / 3 (3xTF32 passes)",
                 "peak_burst": round(pk.get("bf16_tflops", 0) / 6.0, 2),
                 "fp32_simt_peak": round(fp32_peak, 2), "x_fp32_simt_peak": round(achieved / fp32_peak, 3),
                 "kernel": "tf32x3_gemm_kernel (tcgen05.mma kind::tf32, TMEM, TMA)"}
+        if achieved > peak:
+            out["note"] = ("above the ceiling derived from the bf16 sustained figure: that rate was measured "
+                           "under the power cap with bf16 MMAs; tf32 MMAs at the same clock draw less power, "
+                           "so frac against peak_burst is the tighter bound here")
+        return out
     return {"bound": "fp32", "achieved": round(achieved, 2), "peak": round(fp32_peak, 2),
             "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": None,
             "peak_source": fp32_note,
