@@ -130,7 +130,13 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
              int64_t n_rows, int64_t Kp, tc::TcArgs a, cudaStream_t s, char *err, size_t errlen) {
     using Cf = tc::Cfg<BK, BN>;
     CUtensorMap mah, mal, mbh, mbl;
-    const bool ok = a.ilv ? (make_map_ilv(&mah, ahi, m_rows, Kp, tc::BM) && make_map_ilv(&mbh, bhi, n_rows, Kp, BN) &&
+    a.m_tiles = (int)((m_rows + tc::BM - 1) / tc::BM);
+    a.n_tiles = (int)((n_rows + BN - 1) / BN);
+    // 2-CTA clusters over m-tile pairs (the raster keeps pairs on one n-tile
+    // when m_tiles is even): B's half tiles are multicast (TcArgs::pair)
+    a.pair = (a.ilv && a.conv_hw == 0 && a.m_tiles % 2 == 0 && !getenv("LSB_NO_PAIR")) ? 1 : 0;
+    const int b_box = a.pair ? BN / 2 : BN;
+    const bool ok = a.ilv ? (make_map_ilv(&mah, ahi, m_rows, Kp, tc::BM) && make_map_ilv(&mbh, bhi, n_rows, Kp, b_box) &&
                              make_map_ilv(&mal, ahi, m_rows, Kp, tc::BM) && make_map_ilv(&mbl, bhi, n_rows, Kp, BN))
                           : (make_map(&mah, ahi, m_rows, Kp, BK, tc::BM) && make_map(&mal, alo, m_rows, Kp, BK, tc::BM) &&
                              make_map(&mbh, bhi, n_rows, Kp, BK, BN) && make_map(&mbl, blo, n_rows, Kp, BK, BN));
@@ -144,8 +150,6 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
                              (int)Cf::kSmemBytes);
         attr = true;
     }
-    a.m_tiles = (int)((m_rows + tc::BM - 1) / tc::BM);
-    a.n_tiles = (int)((n_rows + BN - 1) / BN);
     dim3 grid((unsigned)(a.m_tiles * a.n_tiles));
     static long long *trace = nullptr;
     const char *trace_path = getenv("LSB_GEMM_TRACE");
@@ -161,11 +165,15 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
         cfg.blockDim = dim3(Cf::kThreads);
         cfg.dynamicSmemBytes = Cf::kSmemBytes;
         cfg.stream = s;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = a.pair ? 2 : 1;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = 2;
         cudaLaunchKernelEx(&cfg, tc::tf32x3_gemm_kernel<BK, BN>, mah, mal, mbh, mbl, a);
     }
     prof_mark(1, s);

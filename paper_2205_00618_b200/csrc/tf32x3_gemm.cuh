@@ -89,6 +89,10 @@ struct TcArgs {
     // (2*Kp floats per row): one 128-B-row SWIZZLE_128B box per operand per
     // stage instead of separate 64-B-row hi and lo boxes (BK = 16 tiles)
     int ilv;
+    // pair: launched as 2-CTA clusters over m-tile pairs that share the n-tile;
+    // each CTA loads half of the B tile and multicasts it to both (B's L2->SM
+    // traffic halves), and each MMA commit frees the slot in both CTAs
+    int pair;
     const int *rowflag, *colflag, *anyflag;   // anyflag[0] A, [1] B
     int *done;                                 // CTA completion counter
     int agen, bgen;
@@ -157,6 +161,29 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *ba
             smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
         : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap *map, uint64_t *bar, void *dst, int x, int y,
+                                               uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
 }
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -522,7 +549,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
         tma_prefetch_desc(&map_blo);
         for (int s = 0; s < STAGES; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], p.pair ? 2 : 1);   // pair: both CTAs' MMAs must be done
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(&tfull[b], 1);
@@ -537,8 +564,10 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     }
     tc_fence_before();
     __syncthreads();
+    if (p.pair) cluster_sync_all();   // partner's barriers initialised before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t crank = p.pair ? cluster_rank() : 0;
 
     if (warp == 0) {
         // ---------------- TMA producer
@@ -555,7 +584,11 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 unsigned char *base = smem + stage * kStageBytes;
                 mbar_expect_tx(&full[stage], kStageBytes);
                 const int kx = kb * BK;
-                if (p.ilv) {   // [A rows: hi16 | lo16][B rows: hi16 | lo16]
+                if (p.ilv && p.pair) {   // own A; half of B (rows crank*BN/2..) into both CTAs
+                    tma_load_2d(&map_ahi, &full[stage], base, 2 * kx, (int)m0);
+                    tma_load_2d_mc(&map_bhi, &full[stage], base + 2 * kTileA + crank * kTileB, 2 * kx,
+                                   (int)(n0 + crank * (BN / 2)), (uint16_t)3);
+                } else if (p.ilv) {   // [A rows: hi16 | lo16][B rows: hi16 | lo16]
                     tma_load_2d(&map_ahi, &full[stage], base, 2 * kx, (int)m0);
                     tma_load_2d(&map_bhi, &full[stage], base + 2 * kTileA, 2 * kx, (int)n0);
                 } else {
@@ -612,7 +645,10 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                     // smem slot free once these MMAs retire; with paired release
                     // one commit per two stages (each commit costs ~45 cycles of
                     // tensor-pipe time, ~5 % of an 810-cycle stage)
-                    if (!kPairRelease || (stage & 1)) umma_commit(&empty[stage]);
+                    if (!kPairRelease || (stage & 1)) {
+                        if (p.pair) umma_commit_mc(&empty[stage], (uint16_t)3);
+                        else umma_commit(&empty[stage]);
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -784,6 +820,8 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::kTmemCols));
     }
     if (p.done != nullptr) tc_nonfinite_fixup(p);
+    // the partner may still commit into this CTA's barriers: leave together
+    if (p.pair) cluster_sync_all();
 }
 
 }  // namespace tc
