@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define LSB_ABI_VERSION 2
+#define LSB_ABI_VERSION 3
 
 /* reduce / combine operators: program.py:182 KIND_CODE */
 enum { LSB_OP_ADD = 0, LSB_OP_MUL = 1, LSB_OP_MAX = 2, LSB_OP_MIN = 3 };
@@ -105,13 +105,23 @@ typedef struct {
     int64_t m_begin, m_end;    /* compute output rows [m_begin, m_end); m_end <= 0 -> M
                                   (row sharding across GPUs) */
     int32_t flags;             /* LSB_GEMM_* bits                          */
-    int32_t reserved;
+    int32_t gen;               /* PREP/PRESPLIT sequences: the caller's nonzero
+                                  generation stamp for non-finite row flags  */
+    int64_t n_begin, n_end;    /* PRESPLIT: output columns [n_begin, n_end)  */
 } lsb_gemm_desc;
 
 /* lsb_gemm_desc.flags: B (pointer, extents, strides and contents) is the same
  * as in the previous lsb_semiring_gemm call on this device -- the 3xTF32 path
  * then reuses its hi/lo split of B (row-block streaming of one contraction) */
 #define LSB_GEMM_B_UNCHANGED 1
+/* Blocked 3xTF32 sequences (execute() overlapping PCIe with compute): split
+ * rows [m_begin, m_end) of A / columns [n_begin, n_end) of B into the
+ * library's full-size split workspace without computing, then compute an
+ * output rectangle from what is already split.  Rectangle corners must be
+ * multiples of the tile (128 rows, 256 columns).  tf32x3 (mul, add) only. */
+#define LSB_GEMM_PREP_A 2
+#define LSB_GEMM_PREP_B 4
+#define LSB_GEMM_PRESPLIT 8
 
 /*
  * Direct 2-D convolution over NCHW-indexed tensors (any element strides),
@@ -185,6 +195,13 @@ int lsb_host_free(void *ptr);
 int lsb_memcpy_h2d(void *dst, const void *src, size_t bytes, void *stream);
 int lsb_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream);
 int lsb_memcpy_d2d(void *dst, const void *src, size_t bytes, void *stream);
+/* pitched host->device copy of `height` rows of `width` bytes (a column
+ * block of a row-major matrix): lets execute() start on B's first column
+ * block while the rest is still crossing PCIe */
+int lsb_memcpy_h2d_2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height,
+                      void *stream);
+int lsb_memcpy_d2h_2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height,
+                      void *stream);
 int lsb_stream_sync(void *stream);
 /* streams / events for overlapping copies with kernels (row-block streaming) */
 int lsb_stream_create(void **stream);

@@ -306,6 +306,28 @@ class Runner:
         fn(blk, stream)
         return native.launch_count() - before
 
+    def descs(self, slots: dict[int, int]):
+        key = tuple(sorted(slots.items()))
+        if key != self._desc_key:
+            self._descs = self._build(slots)
+            self._desc_key = key
+        return self._descs
+
+    def launch_blocked(self, slots: dict[int, int], stream: int, flags: int, gen: int,
+                       r0: int, r1: int, c0: int, c1: int) -> int:
+        """One step of a blocked 3xTF32 sequence (lsb.h LSB_GEMM_PREP_A /
+        PREP_B / PRESPLIT): split A rows [r0, r1) and/or B columns [c0, c1)
+        into the resident split workspace, and/or compute the output
+        rectangle rows [r0, r1) x columns [c0, c1) from what is split."""
+        (fn, d), = self.descs(slots)
+        blk = native.GemmDesc()
+        ctypes.pointer(blk)[0] = d
+        blk.m_begin, blk.m_end, blk.n_begin, blk.n_end = r0, r1, c0, c1
+        blk.flags, blk.gen = flags, gen
+        before = native.launch_count()
+        fn(blk, stream)
+        return native.launch_count() - before
+
     def streams(self):
         if not hasattr(self, "_streams"):
             self._streams = (native.Stream(), native.Stream(), native.Stream())
@@ -403,6 +425,130 @@ def _execute_row_streamed(kernel, r: "Runner", dev, hosts, buffers, rows) -> int
     return launches
 
 
+#: blocked 3xTF32 schedule: pieces per operand (A rows, B columns); piece
+#: sizes are multiples of 256 (the widest output tile)
+BLOCK_PIECES = 8
+_block_gen = [1 << 30]     # sequence ids, disjoint from the library's per-call stamps
+
+
+def _blocked_plan(kernel: CompiledKernel, r: "Runner", dev, hosts: dict):
+    """Blocked schedule for one fp32 (mul, add) GEMM on the 3xTF32 kernel whose
+    A is [M][K] rows of its own slot, B is [K][N] or [N][K] in its own slot and
+    C is [M][N] in its own slot with no C_in; else None."""
+    plan = kernel.plan
+    if os.environ.get("LSB_NO_BLOCKED") or len(plan.steps) != 1 or plan.steps[0].kind != "gemm":
+        return None
+    p = plan.steps[0].params
+    M, N, K = p["M"], p["N"], p["K"]
+    if p["batch"] != 1 or M * N * K < STREAM_MIN_MACS or _reads_c_in(plan):
+        return None
+    if M < 2 * 256 or N < 2 * 256:
+        return None
+    (aref, abase), (bref, bbase), (cref, cbase) = p["A"], p["B"], p["C"]
+    if any(x.kind != "slot" for x in (aref, bref, cref)) or abase or bbase or cbase:
+        return None
+    if len({aref.key, bref.key, cref.key}) != 3 or aref.key not in hosts or bref.key not in hosts:
+        return None
+    size = lambda ref: int(np.prod(plan.slot_shapes[ref.key]))
+    if not (p["sa_k"] == 1 and p["sa_m"] == K and size(aref) == M * K):
+        return None
+    if p["sb_n"] == 1 and p["sb_k"] == N and size(bref) == K * N:
+        b_rowmajor = True          # [K][N]: column pieces are pitched copies
+    elif p["sb_k"] == 1 and p["sb_n"] == K and size(bref) == K * N:
+        b_rowmajor = False         # [N][K]: column pieces are contiguous
+    else:
+        return None
+    if not (p["sc_n"] == 1 and p["sc_m"] == N and size(cref) == M * N):
+        return None
+    (_, d), = r.descs(dev)
+    if native.gemm_algo(d) != "tf32x3":
+        return None
+
+    def pieces(n):
+        per = -(-(-(-n // BLOCK_PIECES)) // 256) * 256
+        return [(x, min(n, x + per)) for x in range(0, n, per)]
+    return dict(M=M, N=N, K=K, a=aref.key, b=bref.key, c=cref.key, b_rowmajor=b_rowmajor,
+                rows=pieces(M), cols=pieces(N))
+
+
+def _execute_blocked(kernel, r: "Runner", dev, hosts, buffers, bp) -> int:
+    """Copy/compute overlap over both operands: A row pieces and B column
+    pieces cross PCIe interleaved (A0 B0 A1 B1 ...); each is split into the
+    resident 3xTF32 workspace as it lands (PREP_A / PREP_B), and as soon as
+    pieces i of A and B are both resident the new L of the output -- rows
+    [0, i] x column piece i, then row piece i x columns [0, i) -- is computed
+    (PRESPLIT) and its rectangles go back to the host as pitched copies while
+    the next pieces upload.  Three streams; PCIe is full duplex."""
+    M, N, K = bp["M"], bp["N"], bp["K"]
+    a_slot, b_slot, c_slot = bp["a"], bp["b"], bp["c"]
+    rows, cols = bp["rows"], bp["cols"]
+    s_in, s_c, s_out = r.streams()
+    for slot, host in hosts.items():
+        if slot not in (a_slot, b_slot, c_slot):
+            native.h2d(dev[slot], host.ctypes.data, host.nbytes, s_in.handle)
+    ahost, bhost = hosts[a_slot], hosts[b_slot]
+    dst = buffers.get(c_slot)
+    direct = (dst is not None and dst.dtype == np.float32 and dst.flags.c_contiguous and dst.flags.writeable)
+    out = dst if direct else np.empty(kernel.slot_shapes[c_slot], np.float32)
+    _block_gen[0] = _block_gen[0] + 1 if _block_gen[0] < (1 << 31) - 2 else 1 << 30
+    gen = _block_gen[0]
+    PA, PB, PS = native.GEMM_PREP_A, native.GEMM_PREP_B, native.GEMM_PRESPLIT
+    launches = 0
+    keep = []
+    nsteps = max(len(rows), len(cols))
+
+    def d2h_rect(r0, r1, c0, c1):
+        native.d2h_2d(out.ctypes.data + 4 * (r0 * N + c0), 4 * N, dev[c_slot] + 4 * (r0 * N + c0), 4 * N,
+                      4 * (c1 - c0), r1 - r0, s_out.handle)
+
+    for i in range(nsteps):
+        ea, eb = native.Event(), native.Event()
+        if i < len(rows):
+            r0, r1 = rows[i]
+            native.h2d(dev[a_slot] + 4 * r0 * K, ahost.ctypes.data + 4 * r0 * K, 4 * (r1 - r0) * K, s_in.handle)
+            ea.record(s_in)
+        if i < len(cols):
+            c0, c1 = cols[i]
+            if bp["b_rowmajor"]:
+                native.h2d_2d(dev[b_slot] + 4 * c0, 4 * N, bhost.ctypes.data + 4 * c0, 4 * N, 4 * (c1 - c0), K,
+                              s_in.handle)
+            else:
+                native.h2d(dev[b_slot] + 4 * c0 * K, bhost.ctypes.data + 4 * c0 * K, 4 * (c1 - c0) * K,
+                           s_in.handle)
+            eb.record(s_in)
+        rects = []
+        if i < len(rows):
+            s_c.wait(ea)
+            launches += r.launch_blocked(dev, s_c.handle, PA, gen, rows[i][0], rows[i][1], 0, 0)
+        if i < len(cols):
+            s_c.wait(eb)
+            launches += r.launch_blocked(dev, s_c.handle, PB, gen, 0, 0, cols[i][0], cols[i][1])
+        ra = min(i + 1, len(rows))      # row pieces resident
+        ca_prev = min(i, len(cols))     # column pieces resident before this step
+        if i < len(cols):               # column piece i against every resident row piece
+            rects.append((0, rows[ra - 1][1], cols[i][0], cols[i][1]))
+        if i < len(rows) and ca_prev:   # row piece i against the earlier column pieces
+            rects.append((rows[i][0], rows[i][1], 0, cols[ca_prev - 1][1]))
+        for (r0, r1, c0, c1) in rects:
+            if r1 <= r0 or c1 <= c0:
+                continue
+            launches += r.launch_blocked(dev, s_c.handle, PS, gen, r0, r1, c0, c1)
+            ec = native.Event()
+            ec.record(s_c)
+            s_out.wait(ec)
+            d2h_rect(r0, r1, c0, c1)
+            keep.append(ec)
+        keep += [ea, eb]
+    s_out.sync()
+    s_c.sync()
+    if not direct:
+        if dst is not None:
+            dst.reshape(-1)[:] = out.reshape(-1).astype(dst.dtype)
+        else:
+            buffers[c_slot] = out
+    return launches
+
+
 def execute(kernel: CompiledKernel, buffers: dict[int, np.ndarray]) -> None:
     """Reference contract (backend.py:121-161): inputs required and never
     mutated, sizes checked (ShapeMismatch), a present output slot is read as
@@ -430,6 +576,12 @@ def execute(kernel: CompiledKernel, buffers: dict[int, np.ndarray]) -> None:
             # absent output read as C_in: zeros (the reference arena is np.zeros)
             n = int(np.prod(kernel.slot_shapes[slot])) if kernel.slot_shapes[slot] else 1
             hosts[slot] = np.zeros(n, np.float32)
+    bp = _blocked_plan(kernel, r, dev, hosts)
+    if bp is not None:
+        launches = _execute_blocked(kernel, r, dev, hosts, buffers, bp)
+        kernel.counters = {k: 0 for k in COUNTERS}
+        kernel.counters["launches"] = launches
+        return
     rows = _row_stream_plan(kernel, hosts)
     if rows is not None:
         launches = _execute_row_streamed(kernel, r, dev, hosts, buffers, rows)

@@ -130,8 +130,11 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
              int64_t n_rows, int64_t Kp, tc::TcArgs a, cudaStream_t s, char *err, size_t errlen) {
     using Cf = tc::Cfg<BK, BN>;
     CUtensorMap mah, mal, mbh, mbl;
-    a.m_tiles = (int)((m_rows + tc::BM - 1) / tc::BM);
-    a.n_tiles = (int)((n_rows + BN - 1) / BN);
+    if (a.m_tiles == 0) {   // the whole output (a blocked launch presets its tile rectangle)
+        a.m_tiles = (int)((m_rows + tc::BM - 1) / tc::BM);
+        a.n_tiles = (int)((n_rows + BN - 1) / BN);
+    }
+    a.bn = BN;
     // 2-CTA clusters over m-tile pairs (the raster keeps pairs on one n-tile
     // when m_tiles is even): B's half tiles are multicast (TcArgs::pair)
     a.pair = (a.ilv && a.conv_hw == 0 && a.m_tiles % 2 == 0 && !getenv("LSB_NO_PAIR")) ? 1 : 0;
@@ -224,6 +227,29 @@ bool tf32x3_supported(int64_t M, int64_t N, int64_t K) {
     return M >= 1 && N >= 1 && K >= 1 && M <= (1ll << 31) && N <= (1ll << 31) && load_encode();
 }
 
+// fast epilogue when every stage is "(+ row-invariant operand[n]) then
+// identity|ReLU" with beta 1 and no C_in (C4's bias + ReLU)
+void set_fast_epilogue(tc::TcArgs &a, const EpiStages &epi) {
+    if (epi.n >= 1 && epi.n <= 2 && !getenv("LSB_NO_FAST_EPI")) {
+        bool ok = true;
+        for (int i = 0; i < epi.n && ok; i++) {
+            const lsb_epi_stage &st = epi.s[i];
+            ok = st.beta == 1.0f && st.alpha == 0.0f && (st.post == LSB_EW_IDENTITY || st.post == LSB_EW_RELU) &&
+                 (st.combine < 0 || (st.combine == LSB_OP_ADD && st.so[1] == 0 && st.operand != nullptr));
+            if (ok) {
+                a.fbias[i] = st.combine < 0 ? nullptr : st.operand;
+                a.fbias_stride[i] = st.so[2];
+                a.frelu[i] = st.post == LSB_EW_RELU;
+            }
+        }
+        if (ok) a.fast_n = epi.n;
+        else {
+            a.fbias[0] = a.fbias[1] = nullptr;
+            a.frelu[0] = a.frelu[1] = 0;
+        }
+    }
+}
+
 // returns 0 on success, else a negative LSB_ERR_* with `err` filled
 int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, int64_t sa_k, const float *B,
                 int64_t sb_k, int64_t sb_n, float *C, int64_t sc_m, int64_t sc_n, int c_vec, const EpiStages &epi,
@@ -305,26 +331,7 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     a.rowflag = rowflag; a.colflag = colflag; a.anyflag = anyflag; a.done = done; a.agen = agen; a.bgen = bgen;
     a.ahi = ahi; a.alo = alo; a.bhi = bhi; a.blo = blo;
     a.ilv = ilv;
-    // fast epilogue when every stage is "(+ row-invariant operand[n]) then
-    // identity|ReLU" with beta 1 and no C_in (C4's bias + ReLU)
-    if (epi.n >= 1 && epi.n <= 2 && !getenv("LSB_NO_FAST_EPI")) {
-        bool ok = true;
-        for (int i = 0; i < epi.n && ok; i++) {
-            const lsb_epi_stage &st = epi.s[i];
-            ok = st.beta == 1.0f && st.alpha == 0.0f && (st.post == LSB_EW_IDENTITY || st.post == LSB_EW_RELU) &&
-                 (st.combine < 0 || (st.combine == LSB_OP_ADD && st.so[1] == 0 && st.operand != nullptr));
-            if (ok) {
-                a.fbias[i] = st.combine < 0 ? nullptr : st.operand;
-                a.fbias_stride[i] = st.so[2];
-                a.frelu[i] = st.post == LSB_EW_RELU;
-            }
-        }
-        if (ok) a.fast_n = epi.n;
-        else {
-            a.fbias[0] = a.fbias[1] = nullptr;
-            a.frelu[0] = a.frelu[1] = 0;
-        }
-    }
+    set_fast_epilogue(a, epi);
     return run_main_cfg(cfg, ahi, alo, bhi, blo, M, N, Kp, a, s, err, errlen);
 }
 
@@ -729,6 +736,114 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
         }
     }
     return LSB_OK;
+}
+
+}  // namespace lsb
+
+namespace lsb {
+
+// Blocked 3xTF32 sequence step (lsb.h LSB_GEMM_PREP_A / PREP_B / PRESPLIT):
+// the split workspace holds the full problem, A rows and B columns are split
+// as they arrive, rectangles computed from what is split.  Coordinates are
+// global; generation d->gen stamps the non-finite flags of the sequence.
+int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec, cudaStream_t s, int *aux_launches,
+                        char *err, size_t errlen) {
+    if (!load_encode()) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
+        return LSB_ERR_UNSUPPORTED;
+    }
+    if (d->gen == 0) {
+        snprintf(err, errlen, "blocked sequences need a nonzero gen");
+        return LSB_ERR_INVALID;
+    }
+    const int64_t M = d->M, N = d->N, K = d->K;
+    constexpr int kKAlign = 32;
+    const int64_t Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
+    const int cfg = pick_cfg(N, K, epi.n > 0);
+    const int ilv = (cfg != 1 && !getenv("LSB_NO_ILV")) ? 1 : 0;
+    const size_t need = sizeof(float) * (size_t)(2 * M + 2 * N) * (size_t)Kp;
+    float *ws;
+    int *flags;
+    {
+        std::lock_guard<std::mutex> lk(g_tc_mu);
+        if (need > g_split_bytes) {
+            if (d->flags & LSB_GEMM_PRESPLIT) {
+                snprintf(err, errlen, "PRESPLIT without a prepared workspace");
+                return LSB_ERR_INVALID;
+            }
+            if (g_split) {
+                cudaDeviceSynchronize();
+                cudaFree(g_split);
+            }
+            g_split = nullptr;
+            g_split_bytes = 0;
+            if (cudaMalloc(&g_split, need) != cudaSuccess) {
+                snprintf(err, errlen, "cudaMalloc(%zu) for the tf32 split operands failed", need);
+                return LSB_ERR_NOMEM;
+            }
+            g_split_bytes = need;
+        }
+        g_bkey = BKey{};   // a blocked sequence owns the workspace
+        ws = g_split;
+        if (M + N + 4 > g_flags_n) {
+            if (g_flags) {
+                cudaDeviceSynchronize();
+                cudaFree(g_flags);
+            }
+            g_flags = nullptr;
+            g_flags_n = 0;
+            if (cudaMalloc(&g_flags, sizeof(int) * (size_t)(M + N + 4)) != cudaSuccess) {
+                snprintf(err, errlen, "cudaMalloc of the non-finite flags failed");
+                return LSB_ERR_NOMEM;
+            }
+            cudaMemsetAsync(g_flags, 0, sizeof(int) * (size_t)(M + N + 4), s);
+            g_flags_n = M + N + 4;
+        }
+        flags = g_flags;
+    }
+    float *bhi = ws, *blo = bhi + N * Kp, *ahi = blo + N * Kp, *alo = ahi + M * Kp;
+    int *anyflag = flags, *done = flags + 2, *colflag = flags + 4, *rowflag = colflag + N;
+    const int64_t rowlen = ilv ? 2 * Kp : Kp;
+    int aux = 0;
+    if (d->flags & LSB_GEMM_PREP_A) {
+        const int64_t r0 = std::max<int64_t>(0, d->m_begin), r1 = d->m_end > 0 ? std::min(d->m_end, M) : M;
+        if (r1 > r0)
+            launch_split(d->A + r0 * d->sa_m, r1 - r0, K, d->sa_m, d->sa_k, ahi + r0 * rowlen, alo + r0 * Kp, Kp, ilv,
+                         rowflag + r0, anyflag, d->gen, s);
+        aux++;
+    }
+    if (d->flags & LSB_GEMM_PREP_B) {
+        const int64_t c0 = std::max<int64_t>(0, d->n_begin), c1 = d->n_end > 0 ? std::min(d->n_end, N) : N;
+        if (c1 > c0)
+            launch_split(d->B + c0 * d->sb_n, c1 - c0, K, d->sb_n, d->sb_k, bhi + c0 * rowlen, blo + c0 * Kp, Kp, ilv,
+                         colflag + c0, anyflag + 1, d->gen, s);
+        aux++;
+    }
+    if (aux_launches) *aux_launches = aux;
+    if (!(d->flags & LSB_GEMM_PRESPLIT)) return LSB_OK;
+
+    const int BN = cfg == 2 ? 256 : 128;
+    const int64_t m0 = std::max<int64_t>(0, d->m_begin), m1 = d->m_end > 0 ? std::min(d->m_end, M) : M;
+    const int64_t n0 = std::max<int64_t>(0, d->n_begin), n1 = d->n_end > 0 ? std::min(d->n_end, N) : N;
+    if (m0 % tc::BM || n0 % BN || (m1 < M && m1 % tc::BM) || (n1 < N && n1 % BN)) {
+        snprintf(err, errlen, "PRESPLIT rectangle must lie on %d x %d tile corners", tc::BM, BN);
+        return LSB_ERR_INVALID;
+    }
+    if (m1 <= m0 || n1 <= n0) return LSB_OK;
+    tc::TcArgs a;
+    memset(&a, 0, sizeof(a));
+    a.M = M; a.N = N; a.K = K; a.Kp = Kp;
+    a.C = d->C; a.sc_m = d->sc_m; a.sc_n = d->sc_n; a.c_vec = c_vec;
+    a.epi = epi;
+    a.rowflag = rowflag; a.colflag = colflag; a.anyflag = anyflag; a.done = done; a.agen = d->gen; a.bgen = d->gen;
+    a.ahi = ahi; a.alo = alo; a.bhi = bhi; a.blo = blo;
+    a.ilv = ilv;
+    a.mt0 = (int)(m0 / tc::BM);
+    a.nt0 = (int)(n0 / BN);
+    a.m_tiles = (int)((m1 - m0 + tc::BM - 1) / tc::BM);
+    a.n_tiles = (int)((n1 - n0 + BN - 1) / BN);
+    set_fast_epilogue(a, epi);
+    return run_main_cfg(cfg, ahi, alo, bhi, blo, M, N, Kp, a, s, err, errlen);
 }
 
 }  // namespace lsb

@@ -237,6 +237,20 @@ int lsb_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream) {
     LSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     return LSB_OK;
 }
+int lsb_memcpy_h2d_2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height,
+                      void *stream) {
+    LSB_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyHostToDevice,
+                               (cudaStream_t)stream));
+    return LSB_OK;
+}
+
+int lsb_memcpy_d2h_2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t height,
+                      void *stream) {
+    LSB_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost,
+                               (cudaStream_t)stream));
+    return LSB_OK;
+}
+
 int lsb_memcpy_d2d(void *dst, const void *src, size_t bytes, void *stream) {
     LSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
     return LSB_OK;
@@ -314,6 +328,23 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     int rc = check_epi(d->n_epi, d->epi);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
+
+    if (d->flags & (LSB_GEMM_PREP_A | LSB_GEMM_PREP_B | LSB_GEMM_PRESPLIT)) {
+        // blocked 3xTF32 sequence step: global coordinates throughout
+        if (d->combine != LSB_OP_MUL || d->reduce != LSB_OP_ADD || d->batch != 1 || d->beta_in_loop ||
+            d->beta != 1.0f || d->K == 0)
+            return fail(LSB_ERR_UNSUPPORTED, "blocked tf32x3 steps cover batch-1 (mul, add) contractions");
+        lsb::EpiStages epi = pack_epi(d->n_epi, d->epi);
+        const int c_vec = (d->sc_n == 1 && aligned16(d->C) && d->sc_m % 4 == 0) ? 1 : 0;
+        char err[256] = "";
+        int aux = 0;
+        rc = lsb::tf32x3_gemm_blocked(d, epi, c_vec, s, &aux, err, sizeof(err));
+        if (rc) return fail(rc, "%s", err);
+        rc = check_launch("tf32x3_gemm_blocked");
+        if (rc) return rc;
+        g_launches.fetch_add(aux + ((d->flags & LSB_GEMM_PRESPLIT) ? 1 : 0), std::memory_order_relaxed);
+        return LSB_OK;
+    }
 
     int64_t m_begin = std::max<int64_t>(0, d->m_begin);
     int64_t m_end = d->m_end > 0 ? std::min(d->m_end, d->M) : d->M;

@@ -33,6 +33,8 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
 int tf32x3_conv(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
 bool tf32x3_conv_direct_ok(const ConvArgs &c, int64_t n_img);
 bool tf32x3_conv_tma_ok(const ConvArgs &c, int64_t n_img);
+int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec, cudaStream_t s, int *aux_launches,
+                        char *err, size_t errlen);
 bool tf32x3_conv_nhwc_ok(const ConvArgs &c, int64_t n_img);
 int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err,
                      size_t errlen);

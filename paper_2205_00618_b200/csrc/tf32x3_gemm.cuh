@@ -63,7 +63,8 @@ constexpr int kGroupM = 16;            // tile raster: 16 m-tiles per group shar
 
 struct TcArgs {
     int64_t M, N, K, Kp;
-    int m_tiles, n_tiles;
+    int m_tiles, n_tiles;   // tiles this launch covers, from tile (mt0, nt0)
+    int mt0, nt0;
     float *C; int64_t sc_m, sc_n;
     int c_vec;
     // conv mode (conv_hw > 0): m = output channel, n = pixel = (img, ho, wo);
@@ -89,6 +90,7 @@ struct TcArgs {
     // (2*Kp floats per row): one 128-B-row SWIZZLE_128B box per operand per
     // stage instead of separate 64-B-row hi and lo boxes (BK = 16 tiles)
     int ilv;
+    int bn;               // the launch's tile width (fixup rectangle)
     // pair: launched as 2-CTA clusters over m-tile pairs that share the n-tile;
     // each CTA loads half of the B tile and multicasts it to both (B's L2->SM
     // traffic halves), and each MMA commit frees the slot in both CTAs
@@ -490,14 +492,17 @@ __device__ void tc_nonfinite_fixup(const TcArgs &p) {
         if (p.epi.n) acc = apply_epilogue(p.epi, acc, 0, m, n, 0);
         p.C[m * p.sc_m + n * p.sc_n] = acc;
     };
+    // this launch's output rectangle (a blocked PRESPLIT launch covers part)
+    const int64_t fm0 = (int64_t)p.mt0 * BM, fm1 = min(p.M, fm0 + (int64_t)p.m_tiles * BM);
+    const int64_t fn0 = (int64_t)p.nt0 * p.bn, fn1 = min(p.N, fn0 + (int64_t)p.n_tiles * p.bn);
     if (fa)
-        for (int64_t m = 0; m < p.M; m++)
+        for (int64_t m = fm0; m < fm1; m++)
             if (p.rowflag[m] == p.agen)
-                for (int64_t n = threadIdx.x; n < p.N; n += blockDim.x) fix(m, n);
+                for (int64_t n = fn0 + threadIdx.x; n < fn1; n += blockDim.x) fix(m, n);
     if (fb)
-        for (int64_t n = 0; n < p.N; n++)
+        for (int64_t n = fn0; n < fn1; n++)
             if (p.colflag[n] == p.bgen)
-                for (int64_t m = threadIdx.x; m < p.M; m += blockDim.x) fix(m, n);
+                for (int64_t m = fm0 + threadIdx.x; m < fm1; m += blockDim.x) fix(m, n);
     if (threadIdx.x == 0) *p.done = 0;
 }
 
@@ -534,8 +539,8 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
         const int g = t / per_group, first_m = g * kGroupM;
         const int gm = min(kGroupM, p.m_tiles - first_m);
         const int r = t % per_group;
-        mt = first_m + r % gm;
-        nt = r / gm;
+        mt = p.mt0 + first_m + r % gm;
+        nt = p.nt0 + r / gm;
     }
     const int64_t m0 = (int64_t)mt * BM, n0 = (int64_t)nt * BN;
     const int num_kb = (int)(p.Kp / BK);

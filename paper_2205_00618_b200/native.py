@@ -19,7 +19,7 @@ LSB_MAX_EPI = 4
 LSB_MAX_NEST_DIMS = 8
 LSB_MAX_NEST_OPERANDS = 4
 LSB_MAX_GUARDS = 4
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 i32, i64, f32, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
 
@@ -45,10 +45,12 @@ class GemmDesc(ctypes.Structure):
                 ("n_epi", i32), ("epi", EpiStage * LSB_MAX_EPI),
                 ("algo", i32), ("split_k", i32), ("tile_m", i32), ("tile_n", i32),
                 ("m_begin", i64), ("m_end", i64),
-                ("flags", i32), ("reserved", i32)]
+                ("flags", i32), ("gen", i32),
+                ("n_begin", i64), ("n_end", i64)]
 
 
 GEMM_B_UNCHANGED = 1
+GEMM_PREP_A, GEMM_PREP_B, GEMM_PRESPLIT = 2, 4, 8
 
 
 class ConvDesc(ctypes.Structure):
@@ -102,6 +104,10 @@ _SIGS = {
     "lsb_memcpy_h2d": ([vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
     "lsb_memcpy_d2h": ([vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
     "lsb_memcpy_d2d": ([vp, vp, ctypes.c_size_t, vp], ctypes.c_int),
+    "lsb_memcpy_h2d_2d": ([vp, ctypes.c_size_t, vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, vp],
+                          ctypes.c_int),
+    "lsb_memcpy_d2h_2d": ([vp, ctypes.c_size_t, vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, vp],
+                          ctypes.c_int),
     "lsb_stream_sync": ([vp], ctypes.c_int),
     "lsb_stream_create": ([ctypes.POINTER(vp)], ctypes.c_int),
     "lsb_stream_destroy": ([vp], ctypes.c_int),
@@ -239,6 +245,16 @@ class PinnedBuffer:
 
 def h2d(dst: int, src: int, nbytes: int, stream: int = 0) -> None:
     check(lib().lsb_memcpy_h2d(vp(dst), vp(src), nbytes, vp(stream)), "lsb_memcpy_h2d")
+
+
+def h2d_2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int, stream: int = 0) -> None:
+    check(lib().lsb_memcpy_h2d_2d(vp(dst), dpitch, vp(src), spitch, width, height, vp(stream)),
+          "lsb_memcpy_h2d_2d")
+
+
+def d2h_2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int, stream: int = 0) -> None:
+    check(lib().lsb_memcpy_d2h_2d(vp(dst), dpitch, vp(src), spitch, width, height, vp(stream)),
+          "lsb_memcpy_d2h_2d")
 
 
 def d2h(dst: int, src: int, nbytes: int, stream: int = 0) -> None:
