@@ -122,6 +122,10 @@ typedef struct {
 #define LSB_GEMM_PREP_A 2
 #define LSB_GEMM_PREP_B 4
 #define LSB_GEMM_PRESPLIT 8
+/* with PRESPLIT: the output region is the L [0, m_end) x [0, n_end) minus
+ * [0, m_begin) x [0, n_begin) -- what becomes computable when the split
+ * pieces grow from (m_begin, n_begin) to (m_end, n_end); one launch */
+#define LSB_GEMM_GROW 16
 
 /*
  * Direct 2-D convolution over NCHW-indexed tensors (any element strides),

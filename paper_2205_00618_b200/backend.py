@@ -425,9 +425,13 @@ def _execute_row_streamed(kernel, r: "Runner", dev, hosts, buffers, rows) -> int
     return launches
 
 
-#: blocked 3xTF32 schedule: pieces per operand (A rows, B columns); piece
-#: sizes are multiples of 256 (the widest output tile)
-BLOCK_PIECES = 8
+#: blocked 3xTF32 schedule: pieces per operand (A rows, B columns), K/1024
+#: clamped to [4, 16] -- long reductions are compute-bound and gain from an
+#: early start (C5: 16 pieces, 53.3 ms vs 54.3 with 8), short ones are
+#: download-bound and lose to per-piece overheads (C4: 4 pieces, 1.9 ms vs
+#: 2.0 with 8 and 2.6 with 16; tools/blocked_timeline.py).  Piece sizes are
+#: multiples of 256 (the widest output tile).  None = that rule.
+BLOCK_PIECES = None
 _block_gen = [1 << 30]     # sequence ids, disjoint from the library's per-call stamps
 
 
@@ -464,8 +468,10 @@ def _blocked_plan(kernel: CompiledKernel, r: "Runner", dev, hosts: dict):
     if native.gemm_algo(d) != "tf32x3":
         return None
 
+    npieces = BLOCK_PIECES or max(4, min(16, K // 1024))
+
     def pieces(n):
-        per = -(-(-(-n // BLOCK_PIECES)) // 256) * 256
+        per = -(-(-(-n // npieces)) // 256) * 256
         return [(x, min(n, x + per)) for x in range(0, n, per)]
     return dict(M=M, N=N, K=K, a=aref.key, b=bref.key, c=cref.key, b_rowmajor=b_rowmajor,
                 rows=pieces(M), cols=pieces(N))
@@ -516,28 +522,47 @@ def _execute_blocked(kernel, r: "Runner", dev, hosts, buffers, bp) -> int:
                 native.h2d(dev[b_slot] + 4 * c0 * K, bhost.ctypes.data + 4 * c0 * K, 4 * (c1 - c0) * K,
                            s_in.handle)
             eb.record(s_in)
-        rects = []
         if i < len(rows):
             s_c.wait(ea)
             launches += r.launch_blocked(dev, s_c.handle, PA, gen, rows[i][0], rows[i][1], 0, 0)
         if i < len(cols):
             s_c.wait(eb)
             launches += r.launch_blocked(dev, s_c.handle, PB, gen, 0, 0, cols[i][0], cols[i][1])
-        ra = min(i + 1, len(rows))      # row pieces resident
-        ca_prev = min(i, len(cols))     # column pieces resident before this step
-        if i < len(cols):               # column piece i against every resident row piece
-            rects.append((0, rows[ra - 1][1], cols[i][0], cols[i][1]))
-        if i < len(rows) and ca_prev:   # row piece i against the earlier column pieces
-            rects.append((rows[i][0], rows[i][1], 0, cols[ca_prev - 1][1]))
-        for (r0, r1, c0, c1) in rects:
-            if r1 <= r0 or c1 <= c0:
-                continue
-            launches += r.launch_blocked(dev, s_c.handle, PS, gen, r0, r1, c0, c1)
+        # resident before / after this step: the new region is the L
+        # [0, m1) x [0, n1) minus [0, m0) x [0, n0)
+        m0 = rows[min(i, len(rows)) - 1][1] if i else 0
+        n0 = cols[min(i, len(cols)) - 1][1] if i else 0
+        m1, n1 = rows[min(i + 1, len(rows)) - 1][1], cols[min(i + 1, len(cols)) - 1][1]
+        strips = [(0, m1, n0, n1), (m0, m1, 0, n0)]
+        strips = [x for x in strips if x[1] > x[0] and x[3] > x[2]]
+        if i < nsteps - 1:
+            # one launch for the whole L (fewer partial waves), then its strips
+            launches += r.launch_blocked(dev, s_c.handle, PS | native.GEMM_GROW, gen, m0, m1, n0, n1)
             ec = native.Event()
             ec.record(s_c)
             s_out.wait(ec)
-            d2h_rect(r0, r1, c0, c1)
+            for x in strips:
+                d2h_rect(*x)
             keep.append(ec)
+        else:
+            # the last L in halves of each strip, each copied back while the
+            # next computes: the tail after the final upload is short
+            for (r0, r1, c0, c1) in strips:
+                if r1 - r0 >= c1 - c0:
+                    mid = r0 + (r1 - r0) // 2 // 256 * 256
+                    parts = [(r0, mid, c0, c1), (mid, r1, c0, c1)]
+                else:
+                    mid = c0 + (c1 - c0) // 2 // 256 * 256
+                    parts = [(r0, r1, c0, mid), (r0, r1, mid, c1)]
+                for x in parts:
+                    if x[1] <= x[0] or x[3] <= x[2]:
+                        continue
+                    launches += r.launch_blocked(dev, s_c.handle, PS, gen, *x)
+                    ec = native.Event()
+                    ec.record(s_c)
+                    s_out.wait(ec)
+                    d2h_rect(*x)
+                    keep.append(ec)
         keep += [ea, eb]
     s_out.sync()
     s_c.sync()

@@ -137,7 +137,7 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
     a.bn = BN;
     // 2-CTA clusters over m-tile pairs (the raster keeps pairs on one n-tile
     // when m_tiles is even): B's half tiles are multicast (TcArgs::pair)
-    a.pair = (a.ilv && a.conv_hw == 0 && a.m_tiles % 2 == 0 && !getenv("LSB_NO_PAIR")) ? 1 : 0;
+    a.pair = (a.ilv && a.conv_hw == 0 && a.m_tiles % 2 == 0 && a.m_tiles2 % 2 == 0 && !getenv("LSB_NO_PAIR")) ? 1 : 0;
     const int b_box = a.pair ? BN / 2 : BN;
     const bool ok = a.ilv ? (make_map_ilv(&mah, ahi, m_rows, Kp, tc::BM) && make_map_ilv(&mbh, bhi, n_rows, Kp, b_box) &&
                              make_map_ilv(&mal, ahi, m_rows, Kp, tc::BM) && make_map_ilv(&mbl, bhi, n_rows, Kp, BN))
@@ -153,7 +153,7 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
                              (int)Cf::kSmemBytes);
         attr = true;
     }
-    dim3 grid((unsigned)(a.m_tiles * a.n_tiles));
+    dim3 grid((unsigned)(a.m_tiles * a.n_tiles + a.m_tiles2 * a.n_tiles2));
     static long long *trace = nullptr;
     const char *trace_path = getenv("LSB_GEMM_TRACE");
     if (trace_path) {
@@ -825,11 +825,16 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
     const int BN = cfg == 2 ? 256 : 128;
     const int64_t m0 = std::max<int64_t>(0, d->m_begin), m1 = d->m_end > 0 ? std::min(d->m_end, M) : M;
     const int64_t n0 = std::max<int64_t>(0, d->n_begin), n1 = d->n_end > 0 ? std::min(d->n_end, N) : N;
-    if (m0 % tc::BM || n0 % BN || (m1 < M && m1 % tc::BM) || (n1 < N && n1 % BN)) {
+    if ((m0 < M && m0 % tc::BM) || (n0 < N && n0 % BN) || (m1 < M && m1 % tc::BM) || (n1 < N && n1 % BN)) {
         snprintf(err, errlen, "PRESPLIT rectangle must lie on %d x %d tile corners", tc::BM, BN);
         return LSB_ERR_INVALID;
     }
-    if (m1 <= m0 || n1 <= n0) return LSB_OK;
+    const bool grow = (d->flags & LSB_GEMM_GROW) != 0;
+    // GROW: [0, m1) x [0, n1) minus [0, m0) x [0, n0) = the column strip
+    // [0, m1) x [n0, n1) plus the row strip [m0, m1) x [0, n0)
+    const int64_t r1m0 = grow ? 0 : m0;
+    const bool has1 = m1 > r1m0 && n1 > n0, has2 = grow && m1 > m0 && n0 > 0;
+    if (!has1 && !has2) return LSB_OK;
     tc::TcArgs a;
     memset(&a, 0, sizeof(a));
     a.M = M; a.N = N; a.K = K; a.Kp = Kp;
@@ -838,10 +843,18 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
     a.rowflag = rowflag; a.colflag = colflag; a.anyflag = anyflag; a.done = done; a.agen = d->gen; a.bgen = d->gen;
     a.ahi = ahi; a.alo = alo; a.bhi = bhi; a.blo = blo;
     a.ilv = ilv;
-    a.mt0 = (int)(m0 / tc::BM);
-    a.nt0 = (int)(n0 / BN);
-    a.m_tiles = (int)((m1 - m0 + tc::BM - 1) / tc::BM);
-    a.n_tiles = (int)((n1 - n0 + BN - 1) / BN);
+    auto rect = [&](int64_t rm0, int64_t rm1, int64_t rn0, int64_t rn1, int &mt, int &nt, int &mts, int &nts) {
+        mt = (int)(rm0 / tc::BM);
+        nt = (int)(rn0 / BN);
+        mts = (int)((rm1 - rm0 + tc::BM - 1) / tc::BM);
+        nts = (int)((rn1 - rn0 + BN - 1) / BN);
+    };
+    if (has1) {
+        rect(r1m0, m1, n0, n1, a.mt0, a.nt0, a.m_tiles, a.n_tiles);
+        if (has2) rect(m0, m1, 0, n0, a.mt2, a.nt2, a.m_tiles2, a.n_tiles2);
+    } else {
+        rect(m0, m1, 0, n0, a.mt0, a.nt0, a.m_tiles, a.n_tiles);
+    }
     set_fast_epilogue(a, epi);
     return run_main_cfg(cfg, ahi, alo, bhi, blo, M, N, Kp, a, s, err, errlen);
 }

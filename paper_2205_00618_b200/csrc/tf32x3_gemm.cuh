@@ -65,6 +65,8 @@ struct TcArgs {
     int64_t M, N, K, Kp;
     int m_tiles, n_tiles;   // tiles this launch covers, from tile (mt0, nt0)
     int mt0, nt0;
+    int m_tiles2, n_tiles2;  // optional second rectangle (blocked L-shaped steps),
+    int mt2, nt2;            // its CTAs follow the first rectangle's
     float *C; int64_t sc_m, sc_n;
     int c_vec;
     // conv mode (conv_hw > 0): m = output channel, n = pixel = (img, ho, wo);
@@ -492,17 +494,22 @@ __device__ void tc_nonfinite_fixup(const TcArgs &p) {
         if (p.epi.n) acc = apply_epilogue(p.epi, acc, 0, m, n, 0);
         p.C[m * p.sc_m + n * p.sc_n] = acc;
     };
-    // this launch's output rectangle (a blocked PRESPLIT launch covers part)
-    const int64_t fm0 = (int64_t)p.mt0 * BM, fm1 = min(p.M, fm0 + (int64_t)p.m_tiles * BM);
-    const int64_t fn0 = (int64_t)p.nt0 * p.bn, fn1 = min(p.N, fn0 + (int64_t)p.n_tiles * p.bn);
-    if (fa)
-        for (int64_t m = fm0; m < fm1; m++)
-            if (p.rowflag[m] == p.agen)
-                for (int64_t n = fn0 + threadIdx.x; n < fn1; n += blockDim.x) fix(m, n);
-    if (fb)
-        for (int64_t n = fn0; n < fn1; n++)
-            if (p.colflag[n] == p.bgen)
-                for (int64_t m = fm0 + threadIdx.x; m < fm1; m += blockDim.x) fix(m, n);
+    // this launch's output rectangles (a blocked PRESPLIT launch covers part)
+    for (int q = 0; q < 2; q++) {
+        const int mt_ = q ? p.mt2 : p.mt0, nt_ = q ? p.nt2 : p.nt0;
+        const int mts = q ? p.m_tiles2 : p.m_tiles, nts = q ? p.n_tiles2 : p.n_tiles;
+        if (mts == 0 || nts == 0) continue;
+        const int64_t fm0 = (int64_t)mt_ * BM, fm1 = min(p.M, fm0 + (int64_t)mts * BM);
+        const int64_t fn0 = (int64_t)nt_ * p.bn, fn1 = min(p.N, fn0 + (int64_t)nts * p.bn);
+        if (fa)
+            for (int64_t m = fm0; m < fm1; m++)
+                if (p.rowflag[m] == p.agen)
+                    for (int64_t n = fn0 + threadIdx.x; n < fn1; n += blockDim.x) fix(m, n);
+        if (fb)
+            for (int64_t n = fn0; n < fn1; n++)
+                if (p.colflag[n] == p.bgen)
+                    for (int64_t m = fm0 + threadIdx.x; m < fm1; m += blockDim.x) fix(m, n);
+    }
     if (threadIdx.x == 0) *p.done = 0;
 }
 
@@ -534,13 +541,17 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     // the next n-tile, so the CTAs resident together share A and B blocks
     int mt, nt;
     {
-        const int t = blockIdx.x;
-        const int per_group = kGroupM * p.n_tiles;
+        int t = blockIdx.x, mtiles = p.m_tiles, ntiles = p.n_tiles, mb = p.mt0, nb = p.nt0;
+        if (t >= p.m_tiles * p.n_tiles) {
+            t -= p.m_tiles * p.n_tiles;
+            mtiles = p.m_tiles2, ntiles = p.n_tiles2, mb = p.mt2, nb = p.nt2;
+        }
+        const int per_group = kGroupM * ntiles;
         const int g = t / per_group, first_m = g * kGroupM;
-        const int gm = min(kGroupM, p.m_tiles - first_m);
+        const int gm = min(kGroupM, mtiles - first_m);
         const int r = t % per_group;
-        mt = p.mt0 + first_m + r % gm;
-        nt = p.nt0 + r / gm;
+        mt = mb + first_m + r % gm;
+        nt = nb + r / gm;
     }
     const int64_t m0 = (int64_t)mt * BM, n0 = (int64_t)nt * BN;
     const int num_kb = (int)(p.Kp / BK);

@@ -50,7 +50,7 @@ class GemmDesc(ctypes.Structure):
 
 
 GEMM_B_UNCHANGED = 1
-GEMM_PREP_A, GEMM_PREP_B, GEMM_PRESPLIT = 2, 4, 8
+GEMM_PREP_A, GEMM_PREP_B, GEMM_PRESPLIT, GEMM_GROW = 2, 4, 8, 16
 
 
 class ConvDesc(ctypes.Structure):
@@ -228,6 +228,7 @@ class PinnedBuffer:
         check(lib().lsb_host_alloc(ctypes.byref(p), max(n, 16)), "lsb_host_alloc")
         self.ptr = int(p.value)
         raw = (ctypes.c_char * max(n, 16)).from_address(self.ptr)
+        raw._owner = self      # the array (via its base) keeps the allocation alive
         self.array = np.frombuffer(raw, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
 
     def close(self) -> None:
