@@ -361,6 +361,31 @@ def roofline(steps, achieved, fp32_peak, sm_max, info, clocks, pk) -> dict:
             "kernel": "semiring_gemm_kernel (SIMT FFMA2 / FADD2+FMNMX3)"}
 
 
+def time_gather(torch, world: int, rows: int, n: int, reps: int = 3) -> dict:
+    """The optional NCCL all-gather of the C row shards: each
+    rank's rows x n f32 shard into the full matrix on every rank, timed on the
+    device (CUDA events, max over ranks).  Not part of `value`."""
+    import torch.distributed as dist
+    local = torch.zeros((rows, n), dtype=torch.float32, device="cuda")
+    out = torch.empty((rows * world, n), dtype=torch.float32, device="cuda")
+    dist.all_gather_into_tensor(out, local)          # warm (communicator, NVLS setup)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        dist.all_gather_into_tensor(out, local)
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / reps], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    recv = (world - 1) * rows * n * 4
+    del local, out
+    return {"ms": round(ms, 4), "bytes_received_per_rank": recv,
+            "algbw_GBps": round(recv / (ms * 1e-3) / 1e9, 1), "collective": "all_gather_into_tensor (NCCL)"}
+
+
 def run_gpu(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -391,6 +416,13 @@ def run_gpu(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms, e2e_ms, _ = t.tolist()
     value = total_flops / (ms * 1e-3) / 1e9
+    gather = None
+    if world > 1 and name == "C5":
+        try:
+            gather = time_gather(torch, world, CONFIGS[name]["M"] // world, CONFIGS[name]["M"])
+            gather["value_with_gather"] = round(total_flops / ((ms + gather["ms"]) * 1e-3) / 1e9, 1)
+        except Exception as e:  # report, never hide
+            gather = {"error": f"{type(e).__name__}: {e}"}
     # roofline numerator: algorithmic flops of the dominant launch / its own
     # average duration (CUDA events around that launch, measured live)
     achieved = flops_rank / (res["kernel_ms"] * 1e-3) / 1e12
@@ -450,6 +482,8 @@ def run_gpu(args):
             "gpu_launches": int(res["launches"]),
             "clocks": clocks,
         }
+        if gather is not None:
+            line["gather"] = gather
         if cpu is not None:
             line["cpu_baseline"] = cpu
         if per_config:

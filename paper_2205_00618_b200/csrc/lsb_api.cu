@@ -518,7 +518,9 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     const bool big = 2.0 * a.M * a.N * d->N * K >= (double)(1ll << 28) && a.M >= 16;
     const bool nhwc_ok = lsb::tf32x3_conv_nhwc_ok(a, d->N);
     const bool tma_ok = lsb::tf32x3_conv_tma_ok(a, d->N), gather_ok = lsb::tf32x3_conv_direct_ok(a, d->N);
-    int tc_mode = big ? (nhwc_ok ? 4 : tma_ok ? 3 : gather_ok ? 1 : 0) : 0;
+    // auto-selection uses only the NHWC kernel: it alone recomputes tiles
+    // with non-finite inputs exactly; the others are on request
+    int tc_mode = big && nhwc_ok ? 4 : 0;
     if (const char *env = getenv("LSB_GEMM_ALGO")) {
         if (!strcmp(env, "simt")) tc_mode = 0;
         else if (!strcmp(env, "tf32x3")) tc_mode = nhwc_ok ? 4 : tma_ok ? 3 : gather_ok ? 1 : 2;

@@ -5,6 +5,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -35,3 +37,21 @@ def test_reference_arm_nonzero_rank_is_silent():
                           "--steps", "1", "--warmup", "0", "--ref-budget", "0.1"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT, env={**os.environ, **e})
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+@pytest.mark.gpu
+def test_bench_gather_timer_single_rank():
+    """The optional C-shard all-gather timer of N>1 runs (bench.time_gather)
+    on a one-rank NCCL group: the code path the 2/4/8-GPU lines take."""
+    code = ("import os, torch, torch.distributed as dist, bench\n"
+            "torch.cuda.set_device(0)\n"
+            "dist.init_process_group('nccl', device_id=torch.device('cuda', 0))\n"
+            "g = bench.time_gather(torch, 1, 1024, 4096)\n"
+            "assert g['ms'] > 0 and g['bytes_received_per_rank'] == 0, g\n"
+            "dist.destroy_process_group()\n"
+            "print('ok')\n")
+    env = {**os.environ, "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": "29517", "RANK": "0", "WORLD_SIZE": "1",
+           "LOCAL_RANK": "0"}
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env=env)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
