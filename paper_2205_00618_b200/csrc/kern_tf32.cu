@@ -43,6 +43,34 @@ int *g_flags = nullptr;
 int64_t g_flags_n = 0;
 int g_gen = 0, g_bgen = 0;
 int *g_conv_flag = nullptr;   // the NHWC conv's "non-finite input" flag (generation-stamped)
+// tail-split partial sums (TcArgs::split_ws) and per-tile arrival counters
+// (zeroed at allocation; each merge re-arms its own)
+float *g_tail_ws = nullptr;
+int *g_tail_cnt = nullptr;
+int64_t g_tail_tiles = 0;
+
+bool ensure_tail_ws(int64_t tiles, cudaStream_t s) {   // slots sized for BN = 256 tiles
+    std::lock_guard<std::mutex> lk(g_tc_mu);
+    if (tiles <= g_tail_tiles) return true;
+    if (g_tail_ws) {
+        cudaDeviceSynchronize();
+        cudaFree(g_tail_ws);
+        cudaFree(g_tail_cnt);
+        g_tail_ws = nullptr;
+        g_tail_cnt = nullptr;
+        g_tail_tiles = 0;
+    }
+    const int64_t t = std::max<int64_t>(tiles, 148);
+    if (cudaMalloc(&g_tail_ws, sizeof(float) * (size_t)t * 2 * tc::BM * 256) != cudaSuccess) return false;
+    if (cudaMalloc(&g_tail_cnt, sizeof(int) * (size_t)t) != cudaSuccess) {
+        cudaFree(g_tail_ws);
+        g_tail_ws = nullptr;
+        return false;
+    }
+    cudaMemsetAsync(g_tail_cnt, 0, sizeof(int) * (size_t)t, s);
+    g_tail_tiles = t;
+    return true;
+}
 
 bool load_encode() {
     if (g_encode) return true;
@@ -130,7 +158,8 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
              int64_t n_rows, int64_t Kp, tc::TcArgs a, cudaStream_t s, char *err, size_t errlen) {
     using Cf = tc::Cfg<BK, BN>;
     CUtensorMap mah, mal, mbh, mbl;
-    if (a.m_tiles == 0) {   // the whole output (a blocked launch presets its tile rectangle)
+    const bool whole = a.m_tiles == 0;
+    if (whole) {   // the whole output (a blocked launch presets its tile rectangle)
         a.m_tiles = (int)((m_rows + tc::BM - 1) / tc::BM);
         a.n_tiles = (int)((n_rows + BN - 1) / BN);
     }
@@ -138,6 +167,23 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
     // 2-CTA clusters over m-tile pairs (the raster keeps pairs on one n-tile
     // when m_tiles is even): B's half tiles are multicast (TcArgs::pair)
     a.pair = (a.ilv && a.conv_hw == 0 && a.m_tiles % 2 == 0 && a.m_tiles2 % 2 == 0 && !getenv("LSB_NO_PAIR")) ? 1 : 0;
+    // tail split: a last wave at most half full runs as twice the CTAs over
+    // half the K chunks each (C4: 512 tiles = 3 waves + 68 -> 444 + 136 halves).
+    // Whole-output GEMM launches only (blocked rectangles keep one order).
+    a.split_tiles = 0;
+    if (whole && a.conv_hw == 0 && !getenv("LSB_NO_TAIL_SPLIT")) {
+        const int T = a.m_tiles * a.n_tiles;
+        const int slots = lsb::device_sms() * Cf::kCtasPerSm;
+        const int rem = T % slots;
+        const int chunks = (int)((Kp / BK + Cf::kChunkStages - 1) / Cf::kChunkStages);
+        const int S = rem + (rem & 1);
+        if (T >= slots && rem > 0 && 2 * rem <= slots && chunks >= 2 && S <= T && (T - S) % 2 == 0 &&
+            ensure_tail_ws(S, s)) {
+            a.split_tiles = S;
+            a.split_ws = g_tail_ws;
+            a.split_cnt = g_tail_cnt;
+        }
+    }
     const int b_box = a.pair ? BN / 2 : BN;
     const bool ok = a.ilv ? (make_map_ilv(&mah, ahi, m_rows, Kp, tc::BM) && make_map_ilv(&mbh, bhi, n_rows, Kp, b_box) &&
                              make_map_ilv(&mal, ahi, m_rows, Kp, tc::BM) && make_map_ilv(&mbl, bhi, n_rows, Kp, BN))
@@ -153,7 +199,7 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
                              (int)Cf::kSmemBytes);
         attr = true;
     }
-    dim3 grid((unsigned)(a.m_tiles * a.n_tiles + a.m_tiles2 * a.n_tiles2));
+    dim3 grid((unsigned)(a.m_tiles * a.n_tiles + a.m_tiles2 * a.n_tiles2 + a.split_tiles));
     static long long *trace = nullptr;
     const char *trace_path = getenv("LSB_GEMM_TRACE");
     if (trace_path) {

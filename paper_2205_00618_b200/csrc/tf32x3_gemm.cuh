@@ -97,6 +97,16 @@ struct TcArgs {
     // each CTA loads half of the B tile and multicasts it to both (B's L2->SM
     // traffic halves), and each MMA commit frees the slot in both CTAs
     int pair;
+    // tail split: the last split_tiles tiles (raster order) run as two CTAs
+    // each over half of the K chunks, so a last wave that would leave most
+    // SMs idle becomes half as long.  CTAs after the first (tiles - split)
+    // come in fours: (tile j, half 0), (tile j+1, half 0), (j, 1), (j+1, 1)
+    // (a 2-CTA pair keeps one n-tile and one K range).  Each half stores
+    // its chunk sum to split_ws; the second to arrive (split_cnt) adds the
+    // other's, runs the epilogue and re-arms the counter.
+    int split_tiles;
+    float *split_ws;
+    int *split_cnt;
     const int *rowflag, *colflag, *anyflag;   // anyflag[0] A, [1] B
     int *done;                                 // CTA completion counter
     int agen, bgen;
@@ -540,8 +550,18 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     // grouped raster: consecutive CTAs walk kGroupM m-tiles before moving to
     // the next n-tile, so the CTAs resident together share A and B blocks
     int mt, nt;
+    int half = -1, stile = 0;   // tail split: K half and split-tile slot
     {
         int t = blockIdx.x, mtiles = p.m_tiles, ntiles = p.n_tiles, mb = p.mt0, nb = p.nt0;
+        if (p.split_tiles) {
+            const int whole = p.m_tiles * p.n_tiles + p.m_tiles2 * p.n_tiles2 - p.split_tiles;
+            if (t >= whole) {
+                const int u = t - whole;
+                stile = (u >> 2) * 2 + (u & 1);
+                half = (u >> 1) & 1;
+                t = whole + stile;
+            }
+        }
         if (t >= p.m_tiles * p.n_tiles) {
             t -= p.m_tiles * p.n_tiles;
             mtiles = p.m_tiles2, ntiles = p.n_tiles2, mb = p.mt2, nb = p.nt2;
@@ -555,7 +575,11 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     }
     const int64_t m0 = (int64_t)mt * BM, n0 = (int64_t)nt * BN;
     const int num_kb = (int)(p.Kp / BK);
-    const int num_chunks = (num_kb + kChunkStages - 1) / kChunkStages;
+    const int all_chunks = (num_kb + kChunkStages - 1) / kChunkStages;
+    // this CTA's K chunks [c_begin, c_begin + num_chunks)
+    const int c_begin = half == 1 ? all_chunks / 2 : 0;
+    const int num_chunks = half < 0 ? all_chunks : half == 0 ? all_chunks / 2 : all_chunks - all_chunks / 2;
+    __shared__ int s_split_second;
     if (threadIdx.x == 0) TC_TRACE(3, 0);
 
     if (warp == 0 && lane == 0) {
@@ -593,7 +617,8 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
             asm volatile("griddepcontrol.wait;" ::: "memory");
             int stage = 0;
             uint32_t phase = 0;
-            for (int kb = 0; kb < num_kb; kb++) {
+            const int kb_end = min(num_kb, (c_begin + num_chunks) * kChunkStages);
+            for (int kb = c_begin * kChunkStages; kb < kb_end; kb++) {
                 // paired release (even STAGES): a slot pair is freed by one
                 // commit after its second stage (see the MMA loop)
                 mbar_wait(&empty[kPairRelease ? (stage | 1) : stage], phase ^ 1);
@@ -631,9 +656,10 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 mbar_wait(&tempty[b], tphase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(b * BN);
-                const int kb_end = min(num_kb, (c + 1) * kChunkStages);
+                const int kb_first = (c_begin + c) * kChunkStages;
+                const int kb_end = min(num_kb, kb_first + kChunkStages);
                 TC_TRACE(2, c);
-                for (int kb = c * kChunkStages; kb < kb_end; kb++) {
+                for (int kb = kb_first; kb < kb_end; kb++) {
                     mbar_wait(&full[stage], phase);
                     TC_TRACE(0, kb);
                     tc_fence_after();
@@ -653,7 +679,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
 #pragma unroll
                     for (int k = 0; k < BK / 8; k++) {
                         const uint64_t off = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along K
-                        const uint32_t first = (kb == c * kChunkStages && k == 0) ? 0u : 1u;
+                        const uint32_t first = (kb == kb_first && k == 0) ? 0u : 1u;
                         umma_tf32(d, ahi + off, bhi + off, idesc, first);
                         umma_tf32(d, ahi + off, blo + off, idesc, 1u);
                         umma_tf32(d, alo + off, bhi + off, idesc, 1u);
@@ -698,6 +724,38 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[b]);
         }
+        bool store = true;
+        if (half >= 0) {
+            // tail split: publish this half's sums (thread-major float4s, a
+            // warp writes 512 contiguous bytes), count arrivals per tile
+            const int et = threadIdx.x - 64;
+            constexpr int kEt = kEpiWarps * 32;
+            float4 *mine = reinterpret_cast<float4 *>(p.split_ws + (size_t)(stile * 2 + half) * (BM * BN));
+#pragma unroll
+            for (int i4 = 0; i4 < 32; i4++)
+                __stcg(mine + i4 * kEt + et, make_float4(tot[i4 * 4], tot[i4 * 4 + 1], tot[i4 * 4 + 2], tot[i4 * 4 + 3]));
+            __threadfence();
+            asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
+            if (et == 0) s_split_second = atomicAdd(p.split_cnt + stile, 1);
+            asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
+            store = s_split_second != 0;
+            if (store) {
+                // the other half is complete: sum in fixed (half 0 + half 1) order
+                __threadfence();
+                const float4 *other =
+                    reinterpret_cast<const float4 *>(p.split_ws + (size_t)(stile * 2 + (half ^ 1)) * (BM * BN));
+#pragma unroll
+                for (int i4 = 0; i4 < 32; i4++) {
+                    const float4 o = __ldcg(other + i4 * kEt + et);
+                    const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        tot[i4 * 4 + e] = half == 1 ? ov[e] + tot[i4 * 4 + e] : tot[i4 * 4 + e] + ov[e];
+                }
+                if (et == 0) p.split_cnt[stile] = 0;   // re-armed for the next launch
+            }
+        }
+        if (store) {
         // stage the tile in (now idle) pipeline smem: row-major, 16-B chunks
         // XOR-swizzled by row so both the write and the read are conflict-free
         float *tile = reinterpret_cast<float *>(smem);
@@ -826,6 +884,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 }
             }
         }
+        }   // store
     }
     if (warp == 2 && lane == 0) TC_TRACE(3, 3);
     tc_fence_before();

@@ -193,3 +193,44 @@ def test_conv_nonfinite(algo, monkeypatch):
     ref = O.reference_eval(gj, ins)
     for s in ref:
         _same(got[s], ref[s], exact=False)
+
+
+@pytest.mark.parametrize("shape", [(2048, 1024, 2560), (4096, 512, 2304), (2176, 200, 4096)])
+def test_tf32x3_tail_split(shape, monkeypatch):
+    """A last wave at most half full runs as two K halves per tile, merged by
+    the second half to finish (TcArgs::split_tiles): 2048x2560 = 160 tiles of
+    128x256 on 148 SMs -> 12 split tiles.  Integer inputs: exact; random
+    normals: the reference metric, and the non-finite fixup still applies."""
+    monkeypatch.setenv("LSB_GEMM_ALGO", "tf32x3")
+    m, k, n = shape
+    gj = _graph("semiring_mul_add", m=m, k=k, n=n)
+    kern, ins = _inputs(gj, 41)
+    got = _run(kern, ins)
+    mvar = [v["id"] for v in json.loads(gj)["vars"] if v["name"] == "m"][0]
+    rows = np.array([0, 1, 127, 128, m // 2, m - 129, m - 2, m - 1])
+    ref = O.reference_eval(gj, ins, restrict={mvar: rows})
+    out = [s for s in ref][0]
+    _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
+    # non-finite rows in split tiles (the last rows of the raster)
+    rng = np.random.default_rng(3)
+    A, B = (rng.standard_normal(ins[s].shape).astype(np.float32) for s in (0, 1))
+    A[m - 1, 3] = np.inf
+    B[1, n - 1] = np.nan
+    got = _run(kern, {0: A, 1: B})
+    ref = O.reference_eval(gj, {0: A, 1: B}, restrict={mvar: rows})
+    # (normal data with K = 1024 fails the strict per-element rule on near-zero
+    # outputs with or without the split -- fp32 accumulation, as in the VM --
+    # so finite values are held to the reference's metric)
+    g = got[out].reshape(m, n)[rows].astype(np.float64)
+    r = np.asarray(ref[out], np.float64).reshape(g.shape)
+    assert np.array_equal(np.isnan(g), np.isnan(r)) and np.array_equal(g[np.isinf(r)], r[np.isinf(r)])
+    fin = np.isfinite(r)
+    assert common.ref_metric(g[fin], r[fin]) <= 1e-4
+    monkeypatch.setenv("LSB_NO_TAIL_SPLIT", "1")
+    plain = _run(kern, {0: A, 1: B})
+    g = np.asarray(got[out], np.float64).reshape(m, n)
+    pl = np.asarray(plain[out], np.float64).reshape(m, n)
+    assert np.array_equal(np.isnan(g), np.isnan(pl))
+    fin = np.isfinite(pl)
+    assert np.array_equal(g[np.isinf(pl)], pl[np.isinf(pl)])
+    assert common.ref_metric(g[fin], pl[fin]) <= 1e-5
