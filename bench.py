@@ -363,27 +363,34 @@ def roofline(steps, achieved, fp32_peak, sm_max, info, clocks, pk) -> dict:
 
 def time_gather(torch, world: int, rows: int, n: int, reps: int = 3) -> dict:
     """The optional NCCL all-gather of the C row shards: each
-    rank's rows x n f32 shard into the full matrix on every rank, timed on the
-    device (CUDA events, max over ranks).  Not part of `value`."""
+    rank's rows x n f32 shard into the full matrix on every rank through the
+    library's lsb_allgather_rows (shard.gather_rows_native), timed on the
+    device (CUDA events on the gather's stream, max over ranks).  Not part of
+    `value`."""
     import torch.distributed as dist
+    from paper_2205_00618_b200 import shard
+    comm = shard.nccl_comm()
     local = torch.zeros((rows, n), dtype=torch.float32, device="cuda")
     out = torch.empty((rows * world, n), dtype=torch.float32, device="cuda")
-    dist.all_gather_into_tensor(out, local)          # warm (communicator, NVLS setup)
+    stream = torch.cuda.current_stream()
+    shard.gather_rows_native(comm, local, out, stream.cuda_stream)   # warm (NVLS setup)
     torch.cuda.synchronize()
     dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
+    a.record(stream)
     for _ in range(reps):
-        dist.all_gather_into_tensor(out, local)
-    b.record()
+        shard.gather_rows_native(comm, local, out, stream.cuda_stream)
+    b.record(stream)
     torch.cuda.synchronize()
     t = torch.tensor([a.elapsed_time(b) / reps], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     recv = (world - 1) * rows * n * 4
     del local, out
+    comm.close()
     return {"ms": round(ms, 4), "bytes_received_per_rank": recv,
-            "algbw_GBps": round(recv / (ms * 1e-3) / 1e9, 1), "collective": "all_gather_into_tensor (NCCL)"}
+            "algbw_GBps": round(recv / (ms * 1e-3) / 1e9, 1),
+            "collective": "lsb_allgather_rows (ncclAllGather, library communicator)"}
 
 
 def run_gpu(args):

@@ -231,6 +231,19 @@ int lsb_affine_nest(const lsb_nest_desc *desc, void *stream);
 int lsb_profile(int enable);
 int lsb_last_kernel_ms(float *ms);
 
+/* ---- optional all-gather of row shards -----------------------
+ * Rank r of P holds rows [r*R, (r+1)*R) of a row-major matrix; the gather
+ * leaves all P*R rows on every rank.  NCCL over NVLink / NVSwitch, loaded at
+ * run time (dlopen libnccl.so.2: the copy torch already loaded when present).
+ * unique id: 128 opaque bytes made on one rank and shared out of band. */
+#define LSB_NCCL_ID_BYTES 128
+int lsb_nccl_unique_id(unsigned char *id /* LSB_NCCL_ID_BYTES */);
+int lsb_nccl_init(int rank, int nranks, const unsigned char *id, void **comm);
+int lsb_nccl_destroy(void *comm);
+/* send: this rank's count floats; recv: nranks*count floats, rank r's block
+ * at recv + r*count; asynchronous on stream */
+int lsb_allgather_rows(void *comm, const float *send, float *recv, int64_t count, void *stream);
+
 /* sizeof of the descriptor structs (which: 0 gemm, 1 conv, 2 nest, 3 epi
  * stage) so bindings can verify their layout without a GPU */
 int64_t lsb_sizeof(int which);

@@ -3,6 +3,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared
 // into paper_2205_00618_b200/liblsb.so (see paper_2205_00618_b200/build.py).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -613,6 +615,91 @@ int lsb_affine_nest(const lsb_nest_desc *d, void *stream) {
     a.epi = pack_epi(d->n_epi, d->epi);
     kNest[d->combine][d->reduce](a, (cudaStream_t)stream);
     return check_launch("affine_nest");
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- NCCL row gather
+// (resolved at run time so liblsb.so has no link-time NCCL dependency; with
+// torch imported first, dlopen returns the libnccl.so.2 torch already mapped)
+namespace {
+struct NcclApi {
+    bool tried = false;
+    void *h = nullptr;
+    ncclResult_t (*get_unique_id)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*all_gather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+int nccl_load() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (!g_nccl.tried) {
+        g_nccl.tried = true;
+        g_nccl.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (g_nccl.h) {
+            g_nccl.get_unique_id = (decltype(g_nccl.get_unique_id))dlsym(g_nccl.h, "ncclGetUniqueId");
+            g_nccl.comm_init_rank = (decltype(g_nccl.comm_init_rank))dlsym(g_nccl.h, "ncclCommInitRank");
+            g_nccl.comm_destroy = (decltype(g_nccl.comm_destroy))dlsym(g_nccl.h, "ncclCommDestroy");
+            g_nccl.all_gather = (decltype(g_nccl.all_gather))dlsym(g_nccl.h, "ncclAllGather");
+            g_nccl.error_string = (decltype(g_nccl.error_string))dlsym(g_nccl.h, "ncclGetErrorString");
+        }
+    }
+    if (!g_nccl.get_unique_id || !g_nccl.comm_init_rank || !g_nccl.comm_destroy || !g_nccl.all_gather)
+        return fail(LSB_ERR_UNSUPPORTED, "libnccl.so.2 not loadable: %s", g_nccl.h ? "missing symbols" : dlerror());
+    return LSB_OK;
+}
+
+int nccl_fail(ncclResult_t r, const char *what) {
+    return fail(LSB_ERR_CUDA, "%s: %s", what, g_nccl.error_string ? g_nccl.error_string(r) : "NCCL error");
+}
+}  // namespace
+
+extern "C" {
+
+int lsb_nccl_unique_id(unsigned char *id) {
+    if (!id) return fail(LSB_ERR_INVALID, "null id");
+    static_assert(sizeof(ncclUniqueId) == LSB_NCCL_ID_BYTES, "ncclUniqueId size");
+    int rc = nccl_load();
+    if (rc) return rc;
+    ncclUniqueId u;
+    ncclResult_t r = g_nccl.get_unique_id(&u);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    memcpy(id, &u, sizeof(u));
+    return LSB_OK;
+}
+
+int lsb_nccl_init(int rank, int nranks, const unsigned char *id, void **comm) {
+    if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(LSB_ERR_INVALID, "bad communicator arguments (rank %d of %d)", rank, nranks);
+    int rc = nccl_load();
+    if (rc) return rc;
+    ncclUniqueId u;
+    memcpy(&u, id, sizeof(u));
+    ncclComm_t c = nullptr;
+    ncclResult_t r = g_nccl.comm_init_rank(&c, nranks, u, rank);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+    *comm = c;
+    return LSB_OK;
+}
+
+int lsb_nccl_destroy(void *comm) {
+    if (!comm) return LSB_OK;
+    int rc = nccl_load();
+    if (rc) return rc;
+    ncclResult_t r = g_nccl.comm_destroy((ncclComm_t)comm);
+    return r == ncclSuccess ? LSB_OK : nccl_fail(r, "ncclCommDestroy");
+}
+
+int lsb_allgather_rows(void *comm, const float *send, float *recv, int64_t count, void *stream) {
+    if (!comm || count < 0 || (count > 0 && (!send || !recv))) return fail(LSB_ERR_INVALID, "bad gather arguments");
+    int rc = nccl_load();
+    if (rc) return rc;
+    ncclResult_t r = g_nccl.all_gather(send, recv, (size_t)count, ncclFloat32, (ncclComm_t)comm, (cudaStream_t)stream);
+    return r == ncclSuccess ? LSB_OK : nccl_fail(r, "ncclAllGather");
 }
 
 }  // extern "C"

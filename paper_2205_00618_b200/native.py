@@ -109,6 +109,10 @@ _SIGS = {
     "lsb_memcpy_d2h_2d": ([vp, ctypes.c_size_t, vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, vp],
                           ctypes.c_int),
     "lsb_stream_sync": ([vp], ctypes.c_int),
+    "lsb_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
+    "lsb_nccl_init": ([ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)], ctypes.c_int),
+    "lsb_nccl_destroy": ([vp], ctypes.c_int),
+    "lsb_allgather_rows": ([vp, vp, vp, i64, vp], ctypes.c_int),
     "lsb_stream_create": ([ctypes.POINTER(vp)], ctypes.c_int),
     "lsb_stream_destroy": ([vp], ctypes.c_int),
     "lsb_event_create": ([ctypes.POINTER(vp)], ctypes.c_int),
@@ -328,3 +332,40 @@ def conv2d_nchw(desc: ConvDesc, stream: int = 0) -> None:
 
 def affine_nest(desc: NestDesc, stream: int = 0) -> None:
     check(lib().lsb_affine_nest(ctypes.byref(desc), vp(stream)), "lsb_affine_nest")
+
+
+NCCL_ID_BYTES = 128
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+    check(lib().lsb_nccl_unique_id(buf), "lsb_nccl_unique_id")
+    return buf.raw
+
+
+class NcclComm:
+    """NCCL communicator owned by the library (lsb_nccl_init); rank/nranks
+    like ncclCommInitRank, the 128-byte id from nccl_unique_id() on one rank."""
+
+    def __init__(self, rank: int, nranks: int, uid: bytes):
+        if len(uid) != NCCL_ID_BYTES:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        p = vp()
+        check(lib().lsb_nccl_init(rank, nranks, uid, ctypes.byref(p)), "lsb_nccl_init")
+        self.handle = int(p.value)
+        self.rank, self.nranks = rank, nranks
+
+    def allgather_rows(self, send: int, recv: int, count: int, stream: int = 0) -> None:
+        check(lib().lsb_allgather_rows(vp(self.handle), vp(send), vp(recv), count, vp(stream)),
+              "lsb_allgather_rows")
+
+    def close(self) -> None:
+        if self.handle and _LIB is not None:
+            _LIB.lsb_nccl_destroy(vp(self.handle))
+        self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -68,3 +68,23 @@ def gather_rows(local, world: int, group=None):
         parts = [torch.empty_like(local) for _ in range(world)]
         dist.all_gather(parts, local.contiguous(), group=group)
     return torch.cat([p[:s] for p, s in zip(parts, sizes)])
+
+
+def nccl_comm(group=None):
+    """The library's own NCCL communicator over the ranks of a torch.distributed
+    group (rank 0 makes the unique id, broadcast as an object): the handle
+    lsb_allgather_rows gathers C row shards with."""
+    import torch.distributed as dist
+    from . import native
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = [native.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return native.NcclComm(rank, world, box[0])
+
+
+def gather_rows_native(comm, local, out, stream: int = 0) -> None:
+    """All-gather equal row shards (contiguous torch CUDA tensors, ``out`` of
+    comm.nranks x local's rows) through lsb_allgather_rows."""
+    if not (local.is_contiguous() and out.is_contiguous()) or out.numel() != local.numel() * comm.nranks:
+        raise ValueError("gather_rows_native needs contiguous equal shards and a nranks-times output")
+    comm.allgather_rows(local.data_ptr(), out.data_ptr(), local.numel(), stream)

@@ -63,3 +63,14 @@ def test_missing_library_fails_loudly(monkeypatch):
     monkeypatch.setattr(native, "LIB_PATH", "/nonexistent/liblsb.so")
     with pytest.raises(native.NativeError, match="no CPU fallback"):
         native.lib()
+
+
+def test_nccl_unique_id_without_gpu():
+    """lsb_nccl_unique_id resolves NCCL at run time (dlopen) and needs no GPU;
+    bad communicator arguments are rejected before NCCL is touched."""
+    a, b = native.nccl_unique_id(), native.nccl_unique_id()
+    assert len(a) == native.NCCL_ID_BYTES and a != b
+    with pytest.raises(native.NativeError, match="bad communicator"):
+        native.NcclComm(2, 2, a)
+    rc = native.lib().lsb_allgather_rows(None, None, None, 4, None)
+    assert rc < 0 and "bad gather" in native.last_error()

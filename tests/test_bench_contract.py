@@ -48,6 +48,14 @@ def test_bench_gather_timer_single_rank():
             "dist.init_process_group('nccl', device_id=torch.device('cuda', 0))\n"
             "g = bench.time_gather(torch, 1, 1024, 4096)\n"
             "assert g['ms'] > 0 and g['bytes_received_per_rank'] == 0, g\n"
+            "from paper_2205_00618_b200 import shard\n"
+            "comm = shard.nccl_comm()\n"
+            "x = torch.arange(12, dtype=torch.float32, device='cuda').reshape(3, 4)\n"
+            "y = torch.empty_like(x)\n"
+            "shard.gather_rows_native(comm, x, y, torch.cuda.current_stream().cuda_stream)\n"
+            "torch.cuda.synchronize()\n"
+            "assert torch.equal(x, y)\n"
+            "comm.close()\n"
             "dist.destroy_process_group()\n"
             "print('ok')\n")
     env = {**os.environ, "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": "29517", "RANK": "0", "WORLD_SIZE": "1",
