@@ -118,7 +118,9 @@ typedef struct {
  * rows [m_begin, m_end) of A / columns [n_begin, n_end) of B into the
  * library's full-size split workspace without computing, then compute an
  * output rectangle from what is already split.  Rectangle corners must be
- * multiples of the tile (128 rows, 256 columns).  tf32x3 (mul, add) only. */
+ * multiples of the tile (128 rows, 256 columns).  tf32x3 (mul, add) only.
+ * A sequence owns the device's split workspace from its first PREP to its
+ * last PRESPLIT: other tf32x3 calls on the device in between invalidate it. */
 #define LSB_GEMM_PREP_A 2
 #define LSB_GEMM_PREP_B 4
 #define LSB_GEMM_PRESPLIT 8

@@ -43,6 +43,24 @@ int *g_flags = nullptr;
 int64_t g_flags_n = 0;
 int g_gen = 0, g_bgen = 0;
 int *g_conv_flag = nullptr;   // the NHWC conv's "non-finite input" flag (generation-stamped)
+
+// g_flags with room for n ints (zeroed when (re)allocated: *fresh); caller
+// holds g_tc_mu
+bool grow_flags(int64_t n, cudaStream_t s, bool *fresh) {
+    if (fresh) *fresh = false;
+    if (n <= g_flags_n) return true;
+    if (g_flags) {
+        cudaDeviceSynchronize();
+        cudaFree(g_flags);
+    }
+    g_flags = nullptr;
+    g_flags_n = 0;
+    if (cudaMalloc(&g_flags, sizeof(int) * (size_t)n) != cudaSuccess) return false;
+    cudaMemsetAsync(g_flags, 0, sizeof(int) * (size_t)n, s);
+    g_flags_n = n;
+    if (fresh) *fresh = true;
+    return true;
+}
 // tail-split partial sums (TcArgs::split_ws) and per-tile arrival counters
 // (zeroed at allocation; each merge re-arms its own)
 float *g_tail_ws = nullptr;
@@ -338,19 +356,12 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     int *colflag, *rowflag, *anyflag, *done, agen, bgen;
     {
         std::lock_guard<std::mutex> lk(g_tc_mu);
-        if (M + N + 4 > g_flags_n) {
-            if (g_flags) {
-                cudaDeviceSynchronize();
-                cudaFree(g_flags);
-            }
-            g_flags = nullptr;
-            g_flags_n = 0;
-            if (cudaMalloc(&g_flags, sizeof(int) * (size_t)(M + N + 4)) != cudaSuccess) {
-                snprintf(err, errlen, "cudaMalloc of the non-finite flags failed");
-                return LSB_ERR_NOMEM;
-            }
-            cudaMemsetAsync(g_flags, 0, sizeof(int) * (size_t)(M + N + 4), s);
-            g_flags_n = M + N + 4;
+        bool fresh = false;
+        if (!grow_flags(M + N + 4, s, &fresh)) {
+            snprintf(err, errlen, "cudaMalloc of the non-finite flags failed");
+            return LSB_ERR_NOMEM;
+        }
+        if (fresh) {
             reuse_b = false;   // B's flags were lost
             g_bkey = BKey{};
         }
@@ -831,19 +842,9 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
         }
         g_bkey = BKey{};   // a blocked sequence owns the workspace
         ws = g_split;
-        if (M + N + 4 > g_flags_n) {
-            if (g_flags) {
-                cudaDeviceSynchronize();
-                cudaFree(g_flags);
-            }
-            g_flags = nullptr;
-            g_flags_n = 0;
-            if (cudaMalloc(&g_flags, sizeof(int) * (size_t)(M + N + 4)) != cudaSuccess) {
-                snprintf(err, errlen, "cudaMalloc of the non-finite flags failed");
-                return LSB_ERR_NOMEM;
-            }
-            cudaMemsetAsync(g_flags, 0, sizeof(int) * (size_t)(M + N + 4), s);
-            g_flags_n = M + N + 4;
+        if (!grow_flags(M + N + 4, s, nullptr)) {
+            snprintf(err, errlen, "cudaMalloc of the non-finite flags failed");
+            return LSB_ERR_NOMEM;
         }
         flags = g_flags;
     }
