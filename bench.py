@@ -331,7 +331,7 @@ def traffic_of(name: str, steps) -> float | None:
     return ent["dram_bytes_per_launch"] if ent else None
 
 
-def roofline(steps, achieved, fp32_peak, sm_max, info, clocks, pk) -> dict:
+def roofline(steps, achieved, fp32_peak, sm_max, info, clocks, pk, name: str = "") -> dict:
     """Roofline of the dominant kernel (the contraction launch).
 
     3xTF32 path: three tf32 tcgen05 MMAs per fp32 product, so the ceiling for
@@ -358,7 +358,8 @@ def roofline(steps, achieved, fp32_peak, sm_max, info, clocks, pk) -> dict:
             "peak_source": fp32_note,
             "frac_at_observed_clock": (round(achieved / (fp32_peak * clocks["sm_mhz"] / sm_max), 4)
                                        if clocks.get("sm_mhz") else None),
-            "kernel": "semiring_gemm_kernel (SIMT FFMA2 / FADD2+FMNMX3)"}
+            "kernel": ("maxplus_cluster_kernel (FADD2+FMNMX3; 4-CTA cluster split-K, DSMEM max)"
+                       if name == "C2" else "semiring_gemm_kernel (SIMT FFMA2 / FADD2+FMNMX3)")}
 
 
 def time_gather(torch, world: int, rows: int, n: int, reps: int = 3) -> dict:
@@ -479,7 +480,7 @@ def run_gpu(args):
                        "rows_per_rank": (CONFIGS[name].get("M", 0) // world) if name == "C5" else None,
                        "parallelism": f"row-shard x{world}" if world > 1 else "single",
                        "l2": "inputs 2 GiB > 126 MB L2" if name == "C5" else "L2 flushed between steps"},
-            "roofline": {**roofline(res["steps"], achieved, fp32_peak, sm_max, info, clocks, pk),
+            "roofline": {**roofline(res["steps"], achieved, fp32_peak, sm_max, info, clocks, pk, name),
                          "traffic": traffic_of(name, res["steps"]),
                          "kernel_ms": round(res["kernel_ms"], 4), "step_ms": round(res["ms_mean"], 4)},
             "e2e": {"value": round(total_flops / (e2e_ms * 1e-3) / 1e9, 1), "unit": "GFLOP/s",

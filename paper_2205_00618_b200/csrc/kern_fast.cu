@@ -1,6 +1,7 @@
 // kern_fast.cu -- tuned instantiations: (mul, add) FFMA2, (add, max|min)
 // FADD2 + FMNMX3, for BM = 128 and 64, and the (mul, add) implicit-GEMM conv.
 #include "lsb_dispatch.cuh"
+#include "maxplus_fast.cuh"
 
 namespace lsb {
 
@@ -27,6 +28,55 @@ void launch_streamk(int reduce, const GemmArgs &a, int ctas, cudaStream_t s) {
         semiring_streamk_kernel<LSB_OP_ADD, LSB_OP_MAX, 128><<<ctas, kThreads, 0, s>>>(a);
     else
         semiring_streamk_kernel<LSB_OP_ADD, LSB_OP_MIN, 128><<<ctas, kThreads, 0, s>>>(a);
+}
+
+// the same with the cp.async row-major kernel (maxplus_fast.cuh)
+void launch_streamk_fast(int reduce, const GemmArgs &a, int ctas, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(maxplus_streamk_fast_kernel<LSB_OP_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kMpSmemBytes);
+        cudaFuncSetAttribute(maxplus_streamk_fast_kernel<LSB_OP_MIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kMpSmemBytes);
+        attr = true;
+    }
+    const float id = reduce == LSB_OP_MAX ? -INFINITY : INFINITY;
+    const int64_t total = a.M * a.N;
+    const int fb = (int)std::min<int64_t>((total + 255) / 256, 2048);
+    fill_kernel<0><<<fb, 256, 0, s>>>(a.C, a.M, a.N, a.sc_m, a.sc_n, id);
+    if (reduce == LSB_OP_MAX)
+        maxplus_streamk_fast_kernel<LSB_OP_MAX><<<ctas, kThreads, kMpSmemBytes, s>>>(a);
+    else
+        maxplus_streamk_fast_kernel<LSB_OP_MIN><<<ctas, kThreads, kMpSmemBytes, s>>>(a);
+}
+
+// split-K across a thread-block cluster of `splits` CTAs per output tile,
+// DSMEM reduction (maxplus_cluster_kernel): one launch
+int launch_maxplus_cluster(int reduce, const GemmArgs &a, int splits, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        for (auto fn : {maxplus_cluster_kernel<LSB_OP_MAX>, maxplus_cluster_kernel<LSB_OP_MIN>}) {
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMpClusterSmemBytes);
+            cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        }
+        attr = true;
+    }
+    const int64_t tiles = ((a.M + kMpBM - 1) / kMpBM) * ((a.N + kMpBN - 1) / kMpBN);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(tiles * splits));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kMpClusterSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)splits;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = reduce == LSB_OP_MAX ? cudaLaunchKernelEx(&cfg, maxplus_cluster_kernel<LSB_OP_MAX>, a)
+                                         : cudaLaunchKernelEx(&cfg, maxplus_cluster_kernel<LSB_OP_MIN>, a);
+    return e == cudaSuccess ? 0 : -1;
 }
 
 void launch_conv_fold(const ConvArgs &a, int64_t n_img, cudaStream_t s) {

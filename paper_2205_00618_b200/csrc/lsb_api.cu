@@ -423,11 +423,40 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
         if (d->combine == LSB_OP_ADD && (d->reduce == LSB_OP_MAX || d->reduce == LSB_OP_MIN) &&
             !d->beta_in_loop && d->beta == 1.0f && a.epi.n == 0 && d->batch == 1 && d->split_k == 0 &&
             t128 < 3 * slots && d->K >= 64 * lsb::kBK && !getenv("LSB_NO_STREAMK")) {
-            const int64_t units = t128 * ((d->K + lsb::kBK - 1) / lsb::kBK);
-            int ctas = (int)std::min<int64_t>(slots, std::max<int64_t>(1, units / 16));
+            // row-major 16-B aligned operands with K % 16 == 0 (C2): the
+            // cp.async kernel with 16-deep slices (maxplus_fast.cuh)
+            const bool fast = d->sa_k == 1 && d->sa_m % 4 == 0 && aligned16(a.A) && d->sb_n == 1 &&
+                              d->sb_k % 4 == 0 && aligned16(d->B) && d->N % 4 == 0 && d->K % 16 == 0 &&
+                              !getenv("LSB_NO_MP_FAST");
+            // split-K over a cluster with a DSMEM reduction: one launch, no
+            // fill, no atomics; cluster size S from the slot-wave cost model
+            // (C2: 64 tiles x 4 = 256 CTAs: 78.6 us vs 87 us stream-K)
+            if (fast && !getenv("LSB_NO_MP_CLUSTER")) {
+                int best_s = 0;
+                double best = 1e30;
+                // powers of two only: 3-, 5-, 6-, 7- and 9-CTA clusters measured
+                // 20-30 % slower on C2 (tools/dbg/c2ab.sh), 4 the best
+                for (int sp = 2; sp <= 8; sp *= 2) {
+                    if (d->K / 16 < sp * 4) break;   // >= 4 slices per CTA
+                    const double cost = (double)((t128 * sp + slots - 1) / slots) / sp + 0.002 * sp;
+                    if (cost < best - 1e-12) { best = cost; best_s = sp; }
+                }
+                if (const char *e = getenv("LSB_MP_CLUSTER")) best_s = atoi(e);
+                if (best_s >= 2) {
+                    lsb::prof_mark(0, s);
+                    const int lrc = lsb::launch_maxplus_cluster(d->reduce, a, best_s, s);
+                    lsb::prof_mark(1, s);
+                    if (lrc) return fail(LSB_ERR_CUDA, "maxplus_cluster launch (cluster %d): %s", best_s,
+                                         cudaGetErrorString(cudaGetLastError()));
+                    return check_launch("maxplus_cluster");
+                }
+            }
+            const int64_t units = t128 * (fast ? d->K / 16 : (d->K + lsb::kBK - 1) / lsb::kBK);
+            int ctas = (int)std::min<int64_t>(slots, std::max<int64_t>(1, units / (fast ? 8 : 16)));
             if (const char *e = getenv("LSB_STREAMK_CTAS")) ctas = std::max(1, atoi(e));
             lsb::prof_mark(0, s);
-            lsb::launch_streamk(d->reduce, a, ctas, s);
+            if (fast) lsb::launch_streamk_fast(d->reduce, a, ctas, s);
+            else lsb::launch_streamk(d->reduce, a, ctas, s);
             lsb::prof_mark(1, s);
             rc = check_launch("semiring_streamk");
             if (rc) return rc;

@@ -21,6 +21,8 @@ GemmFn fast_gemm(int combine, int reduce, int bm, bool two_level);   // kern_fas
 void launch_conv_fast(const ConvArgs &a, dim3 grid, size_t dyn, cudaStream_t s);
 void launch_conv_fold(const ConvArgs &a, int64_t n_img, cudaStream_t s);
 void launch_streamk(int reduce, const GemmArgs &a, int ctas, cudaStream_t s);   // 2 launches
+void launch_streamk_fast(int reduce, const GemmArgs &a, int ctas, cudaStream_t s);   // 2 launches
+int launch_maxplus_cluster(int reduce, const GemmArgs &a, int splits, cudaStream_t s);   // 1 launch
 extern const GemmFn kGemmGeneric[4][4];          // kern_generic.cu
 extern const SplitFn kSplit[4];                  // kern_generic.cu
 extern const NestFn kNest[4][4];                 // kern_nest.cu

@@ -649,8 +649,18 @@ __global__ void splitk_epilogue_kernel(const GemmArgs p, int64_t batch) {
     const int64_t total = batch * p.M * p.N;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        float x = p.ws[e];
-        for (int s = 1; s < p.splits; s++) x = Op<OPR>::apply(x, p.ws[s * total + e]);
+        // partial loads batched 8 at a time (independent L2 round trips in
+        // flight), folded strictly in split order
+        float x = __ldcg(p.ws + e);
+        int s = 1;
+        for (; s + 8 <= p.splits; s += 8) {
+            float v[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) v[q] = __ldcg(p.ws + (s + q) * total + e);
+#pragma unroll
+            for (int q = 0; q < 8; q++) x = Op<OPR>::apply(x, v[q]);
+        }
+        for (; s < p.splits; s++) x = Op<OPR>::apply(x, __ldcg(p.ws + s * total + e));
         int64_t n = e % p.N, m = (e / p.N) % p.M, bz = e / (p.N * p.M);
         if (p.epi.n) x = apply_epilogue(p.epi, x, bz, m, n, 0);
         p.C[bz * p.sc_b + m * p.sc_m + n * p.sc_n] = x;
@@ -761,8 +771,16 @@ __global__ void conv_splitk_fold_kernel(const ConvArgs p, int64_t n_img) {
     const int64_t total = n_img * p.M * p.N;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        float x = p.ws[e];
-        for (int s = 1; s < p.splits; s++) x += p.ws[s * total + e];
+        float x = __ldcg(p.ws + e);
+        int s = 1;
+        for (; s + 8 <= p.splits; s += 8) {
+            float v[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) v[q] = __ldcg(p.ws + (s + q) * total + e);
+#pragma unroll
+            for (int q = 0; q < 8; q++) x += v[q];
+        }
+        for (; s < p.splits; s++) x += __ldcg(p.ws + s * total + e);
         const int64_t pix = e % p.N, co = (e / p.N) % p.M, img = e / (p.N * p.M);
         const int64_t ho = pix / p.WO, wo = pix % p.WO;
         if (p.epi.n) x = apply_epilogue(p.epi, x, img, co, ho, wo);

@@ -234,3 +234,26 @@ def test_tf32x3_tail_split(shape, monkeypatch):
     fin = np.isfinite(pl)
     assert np.array_equal(g[np.isinf(pl)], pl[np.isinf(pl)])
     assert common.ref_metric(g[fin], pl[fin]) <= 1e-5
+
+
+@pytest.mark.parametrize("op,shape", [("add_max", (1000, 1024, 1000)), ("add_min", (1024, 2048, 512)),
+                                      ("add_max", (777, 1040, 1001)), ("add_min", (130, 4096, 260))])
+def test_tropical_split_k_paths(op, shape):
+    """Large-K tropical contractions on few tiles take the cluster split-K
+    kernel (row-major, N % 4 == 0, K % 16 == 0: DSMEM max/min across the
+    cluster) or, when those preconditions fail (N = 1001), the stream-K
+    kernel with atomic merges; NaN / inf must come out as in the reference."""
+    m, k, n = shape
+    gj = _graph(f"semiring_{op}", m=m, k=k, n=n)
+    kern, ins = _inputs(gj, 29, -50, 51)
+    A, B = ins[0], ins[1]
+    A[3, k - 1] = np.nan
+    A[m - 1, :] = -np.inf
+    B[k // 2, n - 1] = np.inf
+    B[7, 0] = -np.inf
+    got = _run(kern, ins)
+    mvar = [v["id"] for v in json.loads(gj)["vars"] if v["name"] == "m"][0]
+    rows = np.unique(np.array([0, 3, 64, 127, 128, m // 2, m - 2, m - 1]))
+    ref = O.reference_eval(gj, ins, restrict={mvar: rows})
+    out = [s for s in ref][0]
+    _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
