@@ -30,7 +30,7 @@ from typing import Optional
 
 import numpy as np
 
-from . import native
+from . import native, render
 from .errors import BlockTooLarge, HasReduction, ShapeMismatch
 from .graph import Graph
 from .planner import Plan, Ref, Step, plan_graph
@@ -67,10 +67,13 @@ class LaunchProgram:
     var_names: list = field(default_factory=list)
 
     def disassemble(self) -> str:
+        """One block per launch: the header, then the loop nest the kernel
+        executes (render.py).  ``algo`` is known once descriptors are built
+        (first execute / run_device)."""
         out = []
         for r in self.instrs:
             algo = r.step.params.get("algo_selected")
-            out.append(f"{r.op} {r.step.describe()}" + (f" algo={algo}" if algo else "") + "\n")
+            out.append(render.render_step(r.step, f"{r.op} {r.step.describe()}" + (f" algo={algo}" if algo else "")))
         return "".join(out)
 
     def encode(self):
@@ -102,6 +105,19 @@ class CompiledKernel:
     def memory_access_count(self) -> int:
         return sum(self.counters.get(k, 0) for k in MEM_COUNTERS)
 
+    def _count(self, launches: int) -> None:
+        """Counters of the last execution (reset per call, like the VM's
+        backend.py:121-161): kernel launches, one ``loop`` per launch and
+        the launches' modeled 16-byte global loads / stores (render.traffic)."""
+        c = {k: 0 for k in COUNTERS}
+        for st in self.plan.steps:
+            ld, stv = render.traffic(st)
+            c["vload"] += ld
+            c["vstore"] += stv
+            c["loop"] += 1
+        c["launches"] = launches
+        self.counters = c
+
     @property
     def runner(self) -> "Runner":
         if self._runner is None:
@@ -118,6 +134,9 @@ def _compile(graph: Graph, target, unroll_limit) -> CompiledKernel:
     plan = plan_graph(graph)
     prog = LaunchProgram([LaunchRecord(f"launch.{s.kind}", s) for s in plan.steps],
                          lanes=getattr(target, "lanes", 32), vregs=getattr(target, "vregs", 255))
+    for st in plan.steps:
+        if st.kind == "gemm":
+            _resolve_algo(st)
     ms = (time.perf_counter() - t0) * 1000.0
     limit = unroll_limit if unroll_limit is not None else getattr(target, "unroll_limit", 0)
     return CompiledKernel(program=prog, target=target, slot_shapes=plan.slot_shapes,
@@ -125,6 +144,21 @@ def _compile(graph: Graph, target, unroll_limit) -> CompiledKernel:
                           scratch_bytes=plan.scratch_bytes, compile_ms=ms,
                           flops=graph.count_flops(), dfg_bytes_moved=graph.bytes_moved(),
                           unroll_limit=limit, counters={k: 0 for k in COUNTERS}, plan=plan)
+
+
+def _resolve_algo(step: Step) -> None:
+    """The algorithm lsb_semiring_gemm will pick (lsb_gemm_algo, host-only
+    heuristics), recorded for disassembly; left unset without the library."""
+    p = step.params
+    d = native.GemmDesc()
+    d.M, d.N, d.K, d.batch = p["M"], p["N"], p["K"], p["batch"]
+    d.combine, d.reduce, d.beta_in_loop = p["combine"], p["reduce"], p["beta_in_loop"]
+    d.algo = p.get("algo", 0)
+    d.m_begin, d.m_end = p.get("m_begin", 0), p.get("m_end", 0)
+    try:
+        p["algo_selected"] = native.gemm_algo(d)
+    except (OSError, native.NativeError):
+        pass
 
 
 def compile_tree(tree, target=None, unroll_limit: Optional[int] = None,
@@ -604,14 +638,12 @@ def execute(kernel: CompiledKernel, buffers: dict[int, np.ndarray]) -> None:
     bp = _blocked_plan(kernel, r, dev, hosts)
     if bp is not None:
         launches = _execute_blocked(kernel, r, dev, hosts, buffers, bp)
-        kernel.counters = {k: 0 for k in COUNTERS}
-        kernel.counters["launches"] = launches
+        kernel._count(launches)
         return
     rows = _row_stream_plan(kernel, hosts)
     if rows is not None:
         launches = _execute_row_streamed(kernel, r, dev, hosts, buffers, rows)
-        kernel.counters = {k: 0 for k in COUNTERS}
-        kernel.counters["launches"] = launches
+        kernel._count(launches)
         return
     for slot, host in hosts.items():
         staged.append(host)
@@ -630,8 +662,7 @@ def execute(kernel: CompiledKernel, buffers: dict[int, np.ndarray]) -> None:
         outs[slot] = res
     native.sync(stream)
     del staged
-    kernel.counters = {k: 0 for k in COUNTERS}
-    kernel.counters["launches"] = launches
+    kernel._count(launches)
     for slot, res in outs.items():
         if slot in buffers:
             dst = buffers[slot]

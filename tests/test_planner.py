@@ -167,3 +167,25 @@ def test_install_rebinds_reference_modules():
     finally:
         P.uninstall()
     assert loopsmith.backend.execute is orig
+
+
+def test_disassemble_renders_balanced_loop_nests():
+    # reference cli.py:56-72 / session.py:247-250 callers look for loop.begin/loop.end
+    for case in IDX["cases"]:
+        k = backend.compile_graph(common.graph_json(case["graph"]))
+        text = k.disassemble()
+        assert text.count("loop.begin") == text.count("loop.end") >= len(k.plan.steps), case["name"]
+
+
+def test_modeled_memory_counters():
+    from paper_2205_00618_b200 import render
+    k = backend.compile_graph(common.graph_json(common.config("C1")["graph"]))
+    (st,) = k.plan.steps
+    ld, sv = render.traffic(st)
+    M = N = K = 256
+    bm = 64 if st.params.get("tile_hint") == 64 else 128
+    assert ld == (K * (M * -(-N // 128) + N * -(-M // bm))) // 4
+    assert sv == M * N // 4
+    k._count(1)
+    assert k.memory_access_count() == ld + sv
+    assert k.counters["launches"] == 1 and k.counters["loop"] == 1

@@ -28,3 +28,15 @@ for c0 in range(0, N, w):
 native.sync(0)
 dt = time.perf_counter() - t
 print(f"h2d_2d (8 column blocks, 8 KiB rows): {4 * K * N / dt / 1e9:.1f} GB/s")
+# full duplex: 1 GiB up and 1 GiB down at the same time on two streams
+h2 = native.PinnedBuffer((n,))
+d2 = native.DeviceBuffer(4 * n)
+s1, s2 = native.Stream(), native.Stream()
+for rep in range(2):
+    native.sync(0)
+    t = time.perf_counter()
+    native.h2d(d.ptr, h.array.ctypes.data, 4 * n, s1.handle)
+    native.d2h(h2.array.ctypes.data, d2.ptr, 4 * n, s2.handle)
+    s1.sync(); s2.sync()
+    dt = time.perf_counter() - t
+print(f"duplex (1 GiB each way concurrently): {2 * 4 * n / dt / 1e9:.1f} GB/s aggregate, {dt * 1e3:.1f} ms")
