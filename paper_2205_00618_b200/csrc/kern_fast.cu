@@ -2,6 +2,7 @@
 // FADD2 + FMNMX3, for BM = 128 and 64, and the (mul, add) implicit-GEMM conv.
 #include "lsb_dispatch.cuh"
 #include "maxplus_fast.cuh"
+#include "small_gemm.cuh"
 
 namespace lsb {
 
@@ -76,6 +77,67 @@ int launch_maxplus_cluster(int reduce, const GemmArgs &a, int splits, cudaStream
     cfg.numAttrs = 1;
     cudaError_t e = reduce == LSB_OP_MAX ? cudaLaunchKernelEx(&cfg, maxplus_cluster_kernel<LSB_OP_MAX>, a)
                                          : cudaLaunchKernelEx(&cfg, maxplus_cluster_kernel<LSB_OP_MIN>, a);
+    return e == cudaSuccess ? 0 : -1;
+}
+
+// latency-bound contractions: one launch, K split across the CTA's warps
+// (small_gemm.cuh).  32 x 16 tiles while 32 x 32 ones would not cover the
+// SMs.  Returns -1 for operator pairs without an instantiation.
+template <int C, int R, int TN>
+static int launch_small_tn(const GemmArgs &a, int64_t batch, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(small_gemm_kernel<C, R, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)SgSmem<TN>::kBytes);
+        attr = true;
+    }
+    const int64_t tiles = ((a.M + kSgTM - 1) / kSgTM) * ((a.N + TN - 1) / TN);
+    small_gemm_kernel<C, R, TN><<<dim3((unsigned)tiles, (unsigned)batch), kSgThreads, SgSmem<TN>::kBytes, s>>>(a);
+    return 0;
+}
+
+template <int C, int R>
+static int launch_small_pair(const GemmArgs &a, int64_t batch, cudaStream_t s) {
+    const int64_t t32 = ((a.M + kSgTM - 1) / kSgTM) * ((a.N + 31) / 32) * batch;
+    return t32 < device_sms() ? launch_small_tn<C, R, 16>(a, batch, s) : launch_small_tn<C, R, 32>(a, batch, s);
+}
+
+int launch_small_gemm(int c, int r, const GemmArgs &a, int64_t batch, cudaStream_t s) {
+    if (c == LSB_OP_MUL && r == LSB_OP_ADD) return launch_small_pair<LSB_OP_MUL, LSB_OP_ADD>(a, batch, s);
+    if (c == LSB_OP_ADD && r == LSB_OP_MAX) return launch_small_pair<LSB_OP_ADD, LSB_OP_MAX>(a, batch, s);
+    if (c == LSB_OP_ADD && r == LSB_OP_MIN) return launch_small_pair<LSB_OP_ADD, LSB_OP_MIN>(a, batch, s);
+    return -1;
+}
+
+// stream-K with the in-kernel fixup (maxplus_fixup_kernel): cooperative
+// launch so every CTA is resident; returns the CTA count used, or -1
+int maxplus_fixup_ctas(int64_t units) {
+    static int occ = -1;
+    if (occ < 0) {
+        for (auto fn : {maxplus_fixup_kernel<LSB_OP_MAX>, maxplus_fixup_kernel<LSB_OP_MIN>})
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMpSmemBytes);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, maxplus_fixup_kernel<LSB_OP_MAX>, kThreads,
+                                                          kMpSmemBytes) != cudaSuccess)
+            occ = 0;
+    }
+    return (int)std::min<int64_t>(units, (int64_t)occ * device_sms());
+}
+
+int launch_maxplus_fixup(int reduce, const GemmArgs &a, int ctas, float4 *part, int *flags, int epoch,
+                         cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kMpSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = reduce == LSB_OP_MAX
+                        ? cudaLaunchKernelEx(&cfg, maxplus_fixup_kernel<LSB_OP_MAX>, a, part, flags, epoch)
+                        : cudaLaunchKernelEx(&cfg, maxplus_fixup_kernel<LSB_OP_MIN>, a, part, flags, epoch);
     return e == cudaSuccess ? 0 : -1;
 }
 

@@ -94,6 +94,36 @@ int workspace(size_t bytes, float **out) {
     return LSB_OK;
 }
 
+// stream-K fixup buffers (maxplus_fixup_kernel): per-CTA partial tiles and
+// epoch-stamped ready flags, zeroed once -- each launch stamps a new epoch,
+// so flags never need a reset launch.  Stream-ordered use, like the split-K
+// workspace: concurrent fixup launches on different streams would share them.
+std::mutex g_fx_mu;
+float4 *g_fx_part = nullptr;
+int *g_fx_flags = nullptr;
+int g_fx_ctas = 0, g_fx_epoch = 0;
+
+int fixup_buffers(int ctas, float4 **part, int **flags, int *epoch) {
+    std::lock_guard<std::mutex> lk(g_fx_mu);
+    if (ctas > g_fx_ctas || g_fx_epoch >= 0x7ffffff0) {
+        cudaDeviceSynchronize();
+        cudaFree(g_fx_part);
+        cudaFree(g_fx_flags);
+        g_fx_part = nullptr;
+        g_fx_flags = nullptr;
+        g_fx_ctas = 0;
+        LSB_CUDA(cudaMalloc(&g_fx_part, sizeof(float4) * 16 * lsb::kThreads * (size_t)ctas));
+        LSB_CUDA(cudaMalloc(&g_fx_flags, sizeof(int) * (size_t)ctas));
+        LSB_CUDA(cudaMemset(g_fx_flags, 0, sizeof(int) * (size_t)ctas));
+        g_fx_ctas = ctas;
+        g_fx_epoch = 0;
+    }
+    *part = g_fx_part;
+    *flags = g_fx_flags;
+    *epoch = ++g_fx_epoch;
+    return LSB_OK;
+}
+
 bool valid_op(int op) { return op >= LSB_OP_ADD && op <= LSB_OP_MIN; }
 bool valid_ew(int ew) { return ew >= LSB_EW_IDENTITY && ew <= LSB_EW_SIGMOID; }
 
@@ -393,6 +423,19 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
         return fail(LSB_ERR_UNSUPPORTED, "K == 0 contraction");
     }
 
+    // latency-bound sizes: one launch, K split across each CTA's warps
+    // (small_gemm.cuh; C1 256^3)
+    if (!d->beta_in_loop && d->beta == 1.0f && d->split_k == 0 && d->K >= 4 &&
+        d->K <= 1024 && d->K % 4 == 0 && d->N % 4 == 0 && (double)M * d->N * d->K * d->batch <= (double)(1 << 26) &&
+        d->sa_k == 1 && d->sa_m % 4 == 0 && aligned16(a.A) && d->sb_n == 1 && d->sb_k % 4 == 0 &&
+        aligned16(d->B) && (d->batch == 1 || (d->sa_b % 4 == 0 && d->sb_b % 4 == 0)) && d->batch <= 65535 &&
+        !getenv("LSB_NO_SMALL")) {
+        lsb::prof_mark(0, s);
+        const int lrc = lsb::launch_small_gemm(d->combine, d->reduce, a, d->batch, s);
+        lsb::prof_mark(1, s);
+        if (lrc == 0) return check_launch("small_gemm");
+    }
+
     GemmFn fn = nullptr;
     int bm = 128;
     if (!d->beta_in_loop) {
@@ -431,7 +474,27 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
             // split-K over a cluster with a DSMEM reduction: one launch, no
             // fill, no atomics; cluster size S from the slot-wave cost model
             // (C2: 64 tiles x 4 = 256 CTAs: 78.6 us vs 87 us stream-K)
-            if (fast && !getenv("LSB_NO_MP_CLUSTER")) {
+            // default: stream-K with the in-kernel fixup (every SM the same
+            // slice count); LSB_MP_MODE=cluster|streamk selects the others
+            const char *mode = getenv("LSB_MP_MODE");
+            if (fast && (!mode || !strcmp(mode, "fixup"))) {
+                const int64_t units = t128 * (d->K / 16);
+                int ctas = lsb::maxplus_fixup_ctas(units);
+                if (const char *e = getenv("LSB_FIXUP_CTAS")) ctas = std::max(1, std::min(ctas, atoi(e)));
+                if (ctas >= 1) {
+                    float4 *part = nullptr;
+                    int *flags = nullptr, epoch = 0;
+                    rc = fixup_buffers(ctas, &part, &flags, &epoch);
+                    if (rc) return rc;
+                    lsb::prof_mark(0, s);
+                    const int lrc = lsb::launch_maxplus_fixup(d->reduce, a, ctas, part, flags, epoch, s);
+                    lsb::prof_mark(1, s);
+                    if (lrc) return fail(LSB_ERR_CUDA, "maxplus_fixup launch (%d CTAs): %s", ctas,
+                                         cudaGetErrorString(cudaGetLastError()));
+                    return check_launch("maxplus_fixup");
+                }
+            }
+            if (fast && !getenv("LSB_NO_MP_CLUSTER") && !(mode && !strcmp(mode, "streamk"))) {
                 int best_s = 0;
                 double best = 1e30;
                 // powers of two only: 3-, 5-, 6-, 7- and 9-CTA clusters measured

@@ -22,6 +22,10 @@ void launch_conv_fast(const ConvArgs &a, dim3 grid, size_t dyn, cudaStream_t s);
 void launch_conv_fold(const ConvArgs &a, int64_t n_img, cudaStream_t s);
 void launch_streamk(int reduce, const GemmArgs &a, int ctas, cudaStream_t s);   // 2 launches
 void launch_streamk_fast(int reduce, const GemmArgs &a, int ctas, cudaStream_t s);   // 2 launches
+int launch_small_gemm(int combine, int reduce, const GemmArgs &a, int64_t batch, cudaStream_t s);   // -1: no kernel
+int maxplus_fixup_ctas(int64_t units);   // co-resident CTA budget (cooperative launch)
+int launch_maxplus_fixup(int reduce, const GemmArgs &a, int ctas, float4 *part, int *flags, int epoch,
+                         cudaStream_t s);   // 1 launch
 int launch_maxplus_cluster(int reduce, const GemmArgs &a, int splits, cudaStream_t s);   // 1 launch
 extern const GemmFn kGemmGeneric[4][4];          // kern_generic.cu
 extern const SplitFn kSplit[4];                  // kern_generic.cu

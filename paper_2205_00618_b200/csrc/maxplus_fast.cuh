@@ -23,9 +23,13 @@
 
 #include "semiring_gemm.cuh"
 
+#ifndef LSB_MP_STAGES
+#define LSB_MP_STAGES 3
+#endif
+
 namespace lsb {
 
-constexpr int kMpBM = 128, kMpBN = 128, kMpBK = 16, kMpStages = 3;
+constexpr int kMpBM = 128, kMpBN = 128, kMpBK = 16, kMpStages = LSB_MP_STAGES;
 constexpr int kMpApitch = kMpBK + 4;   // [m][k] rows of 20 floats (80 B: 16-B aligned, conflict-free)
 constexpr int kMpStageFloats = kMpBM * kMpApitch + kMpBK * kMpBN;
 constexpr size_t kMpSmemBytes = sizeof(float) * kMpStages * kMpStageFloats;
@@ -244,6 +248,99 @@ __global__ void __launch_bounds__(kThreads, 2) maxplus_cluster_kernel(const Gemm
         }
     }
     mp_cluster_sync();   // peers may still read this CTA's partial tile
+}
+
+// stream-K with an in-kernel fixup: a persistent grid of G co-resident CTAs
+// (cooperative launch, 2 per SM) splits the tiles x 16-deep k-slices work
+// into G equal ranges (C2: 4096 units / 296 CTAs, every SM gets the same
+// 27-28 slices -- the cluster split-K leaves 40 SMs with one CTA and the
+// rest with two).  A range is at most two tile segments: the first, if it
+// starts mid-tile, is published as a partial tile (plain stores to a
+// per-CTA workspace slot, then a release flag stamped with the launch
+// epoch); the segment holding a tile's slice 0 is the tile's owner, which
+// after its own slices waits (acquire) on every later CTA whose range
+// reaches into the tile, folds their partials and stores C.  Contributors
+// publish before they wait on anything, so with every CTA resident there
+// is no cycle.  One launch, no fill, no atomics; max/min are exact in any
+// order, so C is bit-identical to the sequential reference.
+__device__ __forceinline__ void mp_flag_release(int *f, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ int mp_flag_acquire(const int *f) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    return v;
+}
+
+template <int OPR>
+__global__ void __launch_bounds__(kThreads, 2) maxplus_fixup_kernel(const GemmArgs p, float4 *part, int *flags,
+                                                                     int epoch) {
+    extern __shared__ __align__(16) float mp_smem[];
+    const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+    const int64_t n_tiles = (p.N + kMpBN - 1) / kMpBN, m_tiles = (p.M + kMpBM - 1) / kMpBM;
+    const int64_t ks = p.K / kMpBK;
+    const int64_t U = m_tiles * n_tiles * ks, G = gridDim.x, b = blockIdx.x;
+    const int64_t u0 = U * b / G, u1 = U * (b + 1) / G;
+    for (int64_t u = u0; u < u1;) {
+        const int64_t tile = u / ks, s0 = u % ks, tile_end = (tile + 1) * ks;
+        const int64_t seg_end = min(u1, tile_end);
+        const int64_t m0 = (tile / n_tiles) * kMpBM, n0 = (tile % n_tiles) * kMpBN;
+        float2 acc[8][4];
+        mp_acc_init<OPR>(acc);
+        mp_tile_slices<OPR>(p, mp_smem, m0, n0, s0 * kMpBK, (int)(seg_end - u), acc);
+        if (s0 != 0) {
+            // contributor: this CTA's (only) partial tile, thread-major float4s
+            float4 *dst = part + b * (16 * kThreads);
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                    __stcg(dst + (i * 2 + h) * kThreads + t,
+                           make_float4(acc[i][2 * h].x, acc[i][2 * h].y, acc[i][2 * h + 1].x, acc[i][2 * h + 1].y));
+            __syncthreads();
+            if (t == 0) {
+                __threadfence();
+                mp_flag_release(flags + b, epoch);
+            }
+        } else {
+            // owner: fold the partials of the later CTAs reaching into the tile
+            for (int64_t c = b + 1; seg_end < tile_end && c < G && U * c / G < tile_end; c++) {
+                if (t == 0)
+                    while (mp_flag_acquire(flags + c) != epoch) __nanosleep(32);
+                __syncthreads();
+                const float4 *src = part + c * (16 * kThreads);
+#pragma unroll
+                for (int i = 0; i < 8; i++)
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const float4 w = __ldcg(src + (i * 2 + h) * kThreads + t);
+                        acc[i][2 * h].x = Op<OPR>::apply(acc[i][2 * h].x, w.x);
+                        acc[i][2 * h].y = Op<OPR>::apply(acc[i][2 * h].y, w.y);
+                        acc[i][2 * h + 1].x = Op<OPR>::apply(acc[i][2 * h + 1].x, w.z);
+                        acc[i][2 * h + 1].y = Op<OPR>::apply(acc[i][2 * h + 1].y, w.w);
+                    }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const int64_t m = m0 + row_of<8>(ty, i);
+                if (m >= p.M) continue;
+                float *dst = p.C + m * p.sc_m;
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const int64_t n = n0 + h * 64 + tx * 4;
+                    const float v[4] = {acc[i][2 * h].x, acc[i][2 * h].y, acc[i][2 * h + 1].x, acc[i][2 * h + 1].y};
+                    if (p.c_vec && n + 3 < p.N) {
+                        *reinterpret_cast<float4 *>(dst + n) = make_float4(v[0], v[1], v[2], v[3]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; q++)
+                            if (n + q < p.N) dst[(n + q) * p.sc_n] = v[q];
+                    }
+                }
+            }
+        }
+        u = seg_end;
+    }
 }
 
 }  // namespace lsb

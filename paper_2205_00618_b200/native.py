@@ -13,7 +13,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblsb.so")
+LIB_PATH = os.environ.get("LSB_LIB_PATH") or os.path.join(PKG, "liblsb.so")   # override: A/B builds (experiments)
 
 LSB_MAX_EPI = 4
 LSB_MAX_NEST_DIMS = 8

@@ -257,3 +257,28 @@ def test_tropical_split_k_paths(op, shape):
     ref = O.reference_eval(gj, ins, restrict={mvar: rows})
     out = [s for s in ref][0]
     _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
+
+
+@pytest.mark.parametrize("mode", ["fixup", "cluster", "streamk"])
+@pytest.mark.parametrize("op,shape", [("add_max", (1024, 1024, 1024)), ("add_min", (777, 1040, 1000)),
+                                      ("add_max", (130, 4096, 260))])
+def test_tropical_underfilled_modes(mode, op, shape, monkeypatch):
+    """The three kernels for underfilled (add, max|min) grids -- stream-K with
+    the in-kernel fixup (default), cluster split-K with DSMEM folds, stream-K
+    with atomic merges (LSB_MP_MODE) -- give the same bytes as the reference,
+    NaN / inf included, wherever the partial boundaries fall."""
+    monkeypatch.setenv("LSB_MP_MODE", mode)
+    m, k, n = shape
+    gj = _graph(f"semiring_{op}", m=m, k=k, n=n)
+    kern, ins = _inputs(gj, 41, -50, 51)
+    A, B = ins[0], ins[1]
+    A[5, k - 3] = np.nan
+    A[m - 1, : k // 3] = -np.inf
+    B[k // 2, n - 1] = np.inf
+    B[k - 1, 17] = np.nan
+    got = _run(kern, ins)
+    mvar = [v["id"] for v in json.loads(gj)["vars"] if v["name"] == "m"][0]
+    rows = np.unique(np.array([0, 5, 127, 128, m // 2, m - 2, m - 1]))
+    ref = O.reference_eval(gj, ins, restrict={mvar: rows})
+    out = [s for s in ref][0]
+    _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
