@@ -706,6 +706,30 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
             if (aux_launches) *aux_launches = 2;
         }
     }
+    // channel-major variant (tf32x3_conv_nhwc_t_kernel): tile_w x tile_h
+    // pixels on the MMA's N (<= 256, a multiple of 16); LSB_CONV_VARIANT=p|t
+    int tw_t = 0, th_t = 0, st_t = 0, sb_t = 0;
+    {
+        const char *cv = getenv("LSB_CONV_VARIANT");
+        bool want = cv ? !strcmp(cv, "t") : false;
+        if (want) {
+            int tw = (int)std::min<int64_t>((c.WO + 7) / 8 * 8, 256 / c.stride_w / 8 * 8);
+            int th = tw > 0 ? (int)std::min<int64_t>({256 / tw, 256 / c.stride_h, c.HO}) : 0;
+            if (const char *e = getenv("LSB_CONV_TW")) tw = atoi(e);   // experiments
+            if (const char *e = getenv("LSB_CONV_TH")) th = atoi(e);
+            while (th > 0 && (tw * th) % 16) th--;
+            const int np = tw * th;
+            if (np >= 64) {
+                const int sb = np * 128 + tc::CN_TILE_B;
+                int st = std::min(tc::CT_MAX_STAGES, (227 * 1024 - 1024 - 256) / sb) & ~1;
+                // epilogue staging: T[128][np + 1] then the dense store box S[64][np]
+                const int64_t stage_need = (((int64_t)128 * (np + 1) + 255) & ~255) * 4 + (int64_t)64 * np * 4;
+                if (st >= 2 && stage_need <= (int64_t)st * sb) {
+                    tw_t = tw; th_t = th; st_t = st; sb_t = sb;
+                }
+            }
+        }
+    }
     CUtensorMap mxs;
     {
         // Xs[n][h][w][cb][32] as 5-D (32, cb, w, h, n); box = one channel block of
@@ -714,7 +738,8 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
         cuuint64_t dims[5] = {32, (cuuint64_t)cbn, (cuuint64_t)c.W, (cuuint64_t)c.H, (cuuint64_t)n_img};
         cuuint64_t strides[4] = {128, (cuuint64_t)cbn * 128, (cuuint64_t)(c.W * cbn) * 128,
                                  (cuuint64_t)(c.H * c.W * cbn) * 128};
-        cuuint32_t box[5] = {32, 1, (cuuint32_t)(32 * c.stride_w), (cuuint32_t)(4 * c.stride_h), 1};
+        cuuint32_t box[5] = {32, 1, (cuuint32_t)((tw_t ? tw_t : 32) * c.stride_w),
+                             (cuuint32_t)((th_t ? th_t : 4) * c.stride_h), 1};
         cuuint32_t estr[5] = {1, 1, (cuuint32_t)c.stride_w, (cuuint32_t)c.stride_h, 1};
         CUresult r = g_encode(&mxs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, xhi, dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -760,8 +785,47 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
         cudaMemsetAsync(trace, 0, (3 * 64 + 3 * 4096) * sizeof(long long), s);
         a.trace = trace;
     }
-    prof_mark(0, s);
-    {
+    if (tw_t) {
+        a.tile_w = tw_t; a.tile_h = th_t; a.npix = tw_t * th_t; a.stages = st_t; a.stage_bytes = sb_t;
+        if (const char *e = getenv("LSB_CT_DBG")) a.dbg = atoi(e);
+        // output by TMA tensor store: NCHW with unit w stride and 16-B strides
+        CUtensorMap mo;
+        memset(&mo, 0, sizeof(mo));
+        if (c.so3 == 1 && c.so2 % 4 == 0 && c.so1 % 4 == 0 && c.so0 % 4 == 0 &&
+            reinterpret_cast<uintptr_t>(c.o) % 16 == 0 && tw_t % 4 == 0 && !getenv("LSB_CT_NO_TMA_OUT")) {
+            cuuint64_t dims[4] = {(cuuint64_t)c.WO, (cuuint64_t)c.HO, (cuuint64_t)CO, (cuuint64_t)n_img};
+            cuuint64_t strides[3] = {(cuuint64_t)c.so2 * 4, (cuuint64_t)c.so1 * 4, (cuuint64_t)c.so0 * 4};
+            cuuint32_t box[4] = {(cuuint32_t)tw_t, (cuuint32_t)th_t, (cuuint32_t)tc::CN_BN, 1};
+            cuuint32_t estr[4] = {1, 1, 1, 1};
+            if (g_encode(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c.o, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+                a.tma_out = 1;
+        }
+        a.tiles_h = (c.HO + th_t - 1) / th_t;
+        a.tiles_w = (c.WO + tw_t - 1) / tw_t;
+        const size_t smem = (size_t)st_t * sb_t + 256 + 1024;
+        static size_t attr_t = 0;
+        if (smem > attr_t) {
+            cudaFuncSetAttribute(tc::tf32x3_conv_nhwc_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_t = smem;
+        }
+        prof_mark(0, s);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(n_img * a.tiles_h * a.tiles_w), (unsigned)co_tiles);
+        cfg.blockDim = dim3(tc::CN_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, tc::tf32x3_conv_nhwc_t_kernel, mxs, mo, a);
+        prof_mark(1, s);
+    }
+    if (!tw_t) {
+        prof_mark(0, s);
         // programmatic dependent launch: the CTAs' setup (barriers, TMEM,
         // descriptor prefetch) overlaps the filter prepass's tail
         cudaLaunchConfig_t cfg = {};
@@ -775,8 +839,8 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         cudaLaunchKernelEx(&cfg, tc::tf32x3_conv_nhwc_kernel, mxs, a);
+        prof_mark(1, s);
     }
-    prof_mark(1, s);
     if (trace_path) {
         static long long h[3 * 64 + 3 * 4096];
         cudaStreamSynchronize(s);

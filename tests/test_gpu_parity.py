@@ -223,3 +223,31 @@ def test_launch_accounting():
     ins, _, _ = common.case_data(case)
     k, _ = _run(common.graph_json(case["graph"]), ins)
     assert native.launch_count() - n0 == len(k.plan.steps) == 3
+
+
+@pytest.mark.parametrize("case", CONV_CASES, ids=[c["name"] for c in CONV_CASES])
+def test_conv_cases_channel_major_variant(case, monkeypatch):
+    """The channel-major NHWC kernel (LSB_CONV_VARIANT=t: filters on the MMA's
+    M, pixels on N, TMA tensor store of the output tile) on the conv fixtures."""
+    monkeypatch.setenv("LSB_CONV_VARIANT", "t")
+    gj = common.graph_json(case["graph"])
+    ins, ref, _ = common.case_data(case)
+    k, got = _run(gj, ins)
+    for slot, r in ref.items():
+        assert common.ref_metric(got[slot], r) <= 1e-4, case["name"]
+        if case["rule"] in ("tol", "exact"):
+            assert common.strict_ok(got[slot], r).all(), case["name"]
+
+
+@pytest.mark.parametrize("store", ["tma", "scalar"])
+def test_c3_channel_major_variant(store, monkeypatch):
+    monkeypatch.setenv("LSB_CONV_VARIANT", "t")
+    if store == "scalar":
+        monkeypatch.setenv("LSB_CT_NO_TMA_OUT", "1")
+    cfg = common.config("C3")
+    bufs = common.config_inputs("C3g")
+    k, got = _run(common.graph_json(cfg["graph_guarded"]), bufs)
+    o = got[2].reshape(8, 64, 56, 56)
+    d = np.load(common.GOLDEN + "/" + cfg["data"])
+    ref0 = d["ref_img0"].astype(np.float64).reshape(64, 56, 56)
+    assert common.strict_ok(o[0], ref0).all()

@@ -100,6 +100,17 @@ __global__ void conv_pattern(int mode, int n_iter, long long *out) {
         const uint32_t i64 = idesc_tf32(128, 64), i128 = idesc_tf32(128, 128), i256 = idesc_tf32(128, 256);
         long long t0 = clock64();
         for (int it = 0; it < n_iter; it++) {
+            if (mode >= 9) {   // mode 9/10/11: channel-major conv stage, A = SW64 filter image
+                               // (128 rows), B = SW128 X box (hi, lo at +64 B), N = 128 / 224 / 256
+                const uint64_t b = sdesc_k_sw<128>(base), a = sdesc_k_sw<64>(base + 32768);
+                const uint32_t id = mode == 9 ? idesc_tf32(128, 128) : mode == 10 ? idesc_tf32(128, 224) : idesc_tf32(128, 256);
+                for (int k = 0; k < 2; k++) {
+                    const uint64_t off = (uint64_t)((k * 32) >> 4);
+                    umma_tf32(tmem, a + off, b + off, id, 1u);
+                    umma_tf32(tmem, a + off, b + 4 + off, id, 1u);
+                }
+                continue;
+            }
             if (mode >= 6) {   // mode 6/7/8: M=64 N=256 / M=64 N=128 / M=128 N=256, 2 per k
                 const uint64_t a = sdesc_k_sw<64>(base), b = sdesc_k_sw<64>(base + 32768);
                 const uint32_t id = mode == 6 ? idesc_tf32(64, 256) : mode == 7 ? idesc_tf32(64, 128) : idesc_tf32(128, 256);
@@ -202,7 +213,7 @@ int main() {
         long long *o2, hh;
         cudaMalloc(&o2, 8);
         cudaFuncSetAttribute(conv_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
-        for (int mode = 0; mode < 9; mode++) {
+        for (int mode = 0; mode < 12; mode++) {
             conv_pattern<<<1, 128, 70000>>>(mode, 200, o2);
             cudaError_t e = cudaDeviceSynchronize();
             cudaMemcpy(&hh, o2, 8, cudaMemcpyDeviceToHost);
