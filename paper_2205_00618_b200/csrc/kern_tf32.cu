@@ -680,32 +680,6 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
         gen = ++g_gen;
         if (gen <= 0) gen = g_gen = 1;
     }
-    {
-        dim3 g((unsigned)((c.W + 31) / 32), (unsigned)((Cp + 31) / 32), (unsigned)(n_img * c.H));
-        const bool vec = c.sx3 == 1 && c.W % 4 == 0 && c.sx0 % 4 == 0 && c.sx1 % 4 == 0 && c.sx2 % 4 == 0 &&
-                         reinterpret_cast<uintptr_t>(c.x) % 16 == 0 &&
-                         (n_img - 1) * c.sx0 + (c.C - 1) * c.sx1 + (c.H - 1) * c.sx2 + c.W < (1ll << 31) &&
-                         (int64_t)xel < (1ll << 31);
-        const int64_t wtot = co_tiles * tc::CN_BN * K;
-        tc::FilterImgArgs f{c.w, CO, K, K, c.C, Cp, c.S, {c.sw0, c.sw1, c.sw2, c.sw3}, wimg};
-        if (vec) {
-            // one launch: X split blocks, then ceil(filter blocks / (gx*gy)) z-slices of filter work
-            const unsigned zsplit = (unsigned)(n_img * ((c.H + tc::kSplitRows - 1) / tc::kSplitRows));
-            const int64_t fblocks = std::min<int64_t>((wtot + 255) / 256, 4096);
-            const unsigned zf = (unsigned)((fblocks + g.x * g.y - 1) / (g.x * g.y));
-            const dim3 gv(g.x, g.y, zsplit + zf);
-            tc::nchw_split_nhwc_vec_kernel<<<gv, 256, 0, s>>>(c.x, (int)c.C, (int)c.H, (int)c.W, (int)Cp, (int)c.sx0,
-                                                              (int)c.sx1, (int)c.sx2, xhi, xlo, anyflag, gen, f,
-                                                              (int)zsplit);
-            if (aux_launches) *aux_launches = 1;
-        } else {
-            tc::nchw_split_nhwc_kernel<<<g, 256, 0, s>>>(c.x, c.C, c.H, c.W, Cp, c.sx0, c.sx1, c.sx2, c.sx3, xhi,
-                                                         xlo, anyflag, gen);
-            tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
-                f, anyflag, gen);
-            if (aux_launches) *aux_launches = 2;
-        }
-    }
     // channel-major variant (tf32x3_conv_nhwc_t_kernel): tile_w x tile_h
     // pixels on the MMA's N (<= 256, a multiple of 16); LSB_CONV_VARIANT=p|t
     int tw_t = 0, th_t = 0, st_t = 0, sb_t = 0;
@@ -722,12 +696,38 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
             if (np >= 64) {
                 const int sb = np * 128 + tc::CN_TILE_B;
                 int st = std::min(tc::CT_MAX_STAGES, (227 * 1024 - 1024 - 256) / sb) & ~1;
-                // epilogue staging: T[128][np + 1] then the dense store box S[64][np]
-                const int64_t stage_need = (((int64_t)128 * (np + 1) + 255) & ~255) * 4 + (int64_t)64 * np * 4;
+                // epilogue staging: S[64][np + 8], then the dense box D[64][np]
+                const int64_t stage_need = ((int64_t)64 * (np + 8) + 255) / 256 * 256 * 4 + (int64_t)64 * np * 4;
                 if (st >= 2 && stage_need <= (int64_t)st * sb) {
                     tw_t = tw; th_t = th; st_t = st; sb_t = sb;
                 }
             }
+        }
+    }
+    {
+        dim3 g((unsigned)((c.W + 31) / 32), (unsigned)((Cp + 31) / 32), (unsigned)(n_img * c.H));
+        const bool vec = c.sx3 == 1 && c.W % 4 == 0 && c.sx0 % 4 == 0 && c.sx1 % 4 == 0 && c.sx2 % 4 == 0 &&
+                         reinterpret_cast<uintptr_t>(c.x) % 16 == 0 &&
+                         (n_img - 1) * c.sx0 + (c.C - 1) * c.sx1 + (c.H - 1) * c.sx2 + c.W < (1ll << 31) &&
+                         (int64_t)xel < (1ll << 31);
+        const int64_t wtot = co_tiles * tc::CN_BN * K;
+        tc::FilterImgArgs f{c.w, CO, K, K, c.C, Cp, c.S, {c.sw0, c.sw1, c.sw2, c.sw3}, wimg, tw_t ? 1 : 0};
+        if (vec) {
+            // one launch: X split blocks, then ceil(filter blocks / (gx*gy)) z-slices of filter work
+            const unsigned zsplit = (unsigned)(n_img * ((c.H + tc::kSplitRows - 1) / tc::kSplitRows));
+            const int64_t fblocks = std::min<int64_t>((wtot + 255) / 256, 4096);
+            const unsigned zf = (unsigned)((fblocks + g.x * g.y - 1) / (g.x * g.y));
+            const dim3 gv(g.x, g.y, zsplit + zf);
+            tc::nchw_split_nhwc_vec_kernel<<<gv, 256, 0, s>>>(c.x, (int)c.C, (int)c.H, (int)c.W, (int)Cp, (int)c.sx0,
+                                                              (int)c.sx1, (int)c.sx2, xhi, xlo, anyflag, gen, f,
+                                                              (int)zsplit);
+            if (aux_launches) *aux_launches = 1;
+        } else {
+            tc::nchw_split_nhwc_kernel<<<g, 256, 0, s>>>(c.x, c.C, c.H, c.W, Cp, c.sx0, c.sx1, c.sx2, c.sx3, xhi,
+                                                         xlo, anyflag, gen);
+            tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
+                f, anyflag, gen);
+            if (aux_launches) *aux_launches = 2;
         }
     }
     CUtensorMap mxs;

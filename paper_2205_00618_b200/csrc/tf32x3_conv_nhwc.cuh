@@ -434,15 +434,16 @@ __global__ void __launch_bounds__(CN_THREADS, 2)
 // pixels (K-major SW128 rows [hi16 | lo16], B_lo = B_hi + 64 B).  Per 8
 // channels two MMAs of 128 x npix x 8:
 //     D += [Whi; Wlo] . Xhi      D += [Whi; Wlo] . Xlo
-// so TMEM rows 0-63 collect Whi.(Xhi + Xlo) and rows 64-127 Wlo.(Xhi + Xlo);
-// the epilogue adds row co and row 64 + co (4 split terms, lo.lo included).
+// so for channel co = 16q + c TMEM row 32q + 2c collects Whi.(Xhi + Xlo) and
+// row 32q + 2c + 1 Wlo.(Xhi + Xlo) (the filter image interleaves the hi and
+// lo rows of a channel, FilterImgArgs::ilv_rows); the epilogue adds them
+// with one warp shuffle (4 split terms, lo.lo included).
 // Why: a 128 x N x 8 tf32 MMA costs ~87 cycles for any N <= 128 and ~135 at
 // N = 256 (tools/umma_mn_test.cu), so the pixel-major kernel's N = 64 + N = 128
 // pair spends 348 cycles per 16 channels on 128 pixels, this one ~2 x 2 x 125
 // on 224 (C3: a 4 x 56 pixel tile, 112 tiles, one CTA per SM).
-// Epilogue: TMEM -> smem T[128][npix + 1] (odd pitch: conflict-free both
-// ways), then warps sweep (co, output row) pairs with lanes along w: the
-// NCHW stores are row-contiguous.
+// Epilogue: TMEM -> shuffle sum -> dense smem box S[64][npix] -> one TMA
+// tensor store into NCHW (or row stores when the strides do not allow it).
 constexpr int CT_MAX_STAGES = 8;
 
 __global__ void __launch_bounds__(CN_THREADS, 1)
@@ -550,16 +551,24 @@ __global__ void __launch_bounds__(CN_THREADS, 1)
         }
     } else {
         // ---------------- epilogue (warps 2..9)
+        // A rows are interleaved per channel (filter image ilv_rows): TMEM
+        // lane 32q + 2c holds Whi.X and lane 32q + 2c + 1 Wlo.X of channel
+        // 16q + c, so one shuffle sums them inside the warp that owns the
+        // lane quarter; even lanes then write S[co][pix] (dense NCHW box).
         const int ew = warp - 2;
         asm volatile("griddepcontrol.wait;" ::: "memory");
         mbar_wait(tdone, 0);
         if (ew == 0 && lane == 0) CN_TRACE(2, 0);
         tc_fence_after();
-        float *T = reinterpret_cast<float *>(smem);   // [128][NP + 1]
-        const int pitch = NP + 1;
-        {
+        // S[64][NP + 8]: a channel's tile rows dense (one TMA box per channel);
+        // the 8-float pad puts the 8 float4 stores of a quarter-warp (4
+        // channels x 2 lanes) in 8 distinct bank groups
+        const int SP = NP + 8;
+        float *S = reinterpret_cast<float *>(smem);
+        const bool nonfinite = *p.anyflag == p.gen;
+        if (!nonfinite) {
             const int qd = warp & 3, half = ew >> 2;
-            const int row = qd * 32 + lane;
+            const int co_l = 16 * qd + (lane >> 1);
             const int nch = (num_kb + p.stages_per_chunk - 1) / p.stages_per_chunk;
             for (int part = half; part < NP / 16; part += 2) {
                 const int col = part * 16;
@@ -569,13 +578,31 @@ __global__ void __launch_bounds__(CN_THREADS, 1)
                     if (ch < nch)
                         tmem_ld16_issue(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ch * 256 + col), rr[ch]);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                float v[16];
 #pragma unroll
                 for (int i = 0; i < 16; i++) {
                     float acc = __uint_as_float(rr[0][i]);
 #pragma unroll
                     for (int ch = 1; ch < CN_CHUNKS; ch++)
                         if (ch < nch) acc += __uint_as_float(rr[ch][i]);
-                    T[row * pitch + col + i] = acc;
+                    v[i] = acc + __shfl_xor_sync(0xffffffffu, acc, 1);   // hi row + lo row
+                }
+                // both lanes of the pair hold the sums: lane half h stores
+                // float4s h and h + 2 of the 16 columns
+                const int h4 = (lane & 1) * 4;
+#pragma unroll
+                for (int q = 0; q < 2; q++) {
+                    float x[4];
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        // static register index: select between the two halves
+                        x[e] = (lane & 1) ? v[q * 8 + 4 + e] : v[q * 8 + e];
+                        if (p.epi.n) {
+                            const int pix = col + q * 8 + h4 + e;
+                            x[e] = apply_epilogue(p.epi, x[e], n, c0 + co_l, h0 + pix / p.tile_w, w0 + pix % p.tile_w);
+                        }
+                    }
+                    *reinterpret_cast<float4 *>(S + co_l * SP + col + q * 8 + h4) = make_float4(x[0], x[1], x[2], x[3]);
                 }
             }
         }
@@ -583,77 +610,77 @@ __global__ void __launch_bounds__(CN_THREADS, 1)
         tc_fence_before();
         asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
         if (ew == 0 && lane == 0) CN_TRACE(2, 4);
-        if (*p.anyflag == p.gen) {
-            if (ew == 0 && lane == 0) CN_TRACE(2, 6);
-            // non-finite input somewhere: FP32 recompute (rows 64.. zeroed)
+        if (nonfinite) {
+            // non-finite input somewhere: FP32 recompute of the tile
             for (int i = threadIdx.x - 64; i < CN_BN * NP; i += CN_EPI_WARPS * 32) {
                 const int co_l = i / NP, pix = i % NP;
                 const int ho = h0 + pix / p.tile_w, wo = w0 + pix % p.tile_w;
                 const int64_t co = c0 + co_l;
-                T[(CN_BN + co_l) * pitch + pix] = 0.0f;
-                if (co >= p.CO || ho >= p.HO || wo >= p.WO) continue;
                 float acc = 0.0f;
-                for (int64_t c = 0; c < p.C; c++)
-                    for (int64_t r = 0; r < p.R; r++) {
-                        const int64_t hi_ = ho * p.sh - p.ph + r * p.dh;
-                        for (int64_t s2 = 0; s2 < p.S; s2++) {
-                            const int64_t wi = wo * p.sw - p.pw + s2 * p.dw;
-                            const bool in = hi_ >= 0 && hi_ < p.H && wi >= 0 && wi < p.W;
-                            const float xv = in ? p.x[n * p.sx[0] + c * p.sx[1] + hi_ * p.sx[2] + wi * p.sx[3]] : 0.0f;
-                            acc = fmaf(xv, p.w[co * p.swt[0] + c * p.swt[1] + r * p.swt[2] + s2 * p.swt[3]], acc);
+                if (co < p.CO && ho < p.HO && wo < p.WO) {
+                    for (int64_t c = 0; c < p.C; c++)
+                        for (int64_t r = 0; r < p.R; r++) {
+                            const int64_t hi_ = ho * p.sh - p.ph + r * p.dh;
+                            for (int64_t s2 = 0; s2 < p.S; s2++) {
+                                const int64_t wi = wo * p.sw - p.pw + s2 * p.dw;
+                                const bool in = hi_ >= 0 && hi_ < p.H && wi >= 0 && wi < p.W;
+                                const float xv =
+                                    in ? p.x[n * p.sx[0] + c * p.sx[1] + hi_ * p.sx[2] + wi * p.sx[3]] : 0.0f;
+                                acc = fmaf(xv, p.w[co * p.swt[0] + c * p.swt[1] + r * p.swt[2] + s2 * p.swt[3]], acc);
+                            }
                         }
-                    }
-                T[co_l * pitch + pix] = acc;
+                    if (p.epi.n) acc = apply_epilogue(p.epi, acc, n, co, ho, wo);
+                }
+                S[co_l * SP + pix] = acc;
             }
             asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
         }
         if (ew == 0 && lane == 0) CN_TRACE(2, 5);
         if (p.tma_out) {
-            // S[co][pix] dense (after T), fused stages, one TMA tensor store
-            float *S = T + ((128 * pitch + 255) & ~255);
-            for (int co_l = ew; co_l < CN_BN; co_l += CN_EPI_WARPS) {
-                const float *t0 = T + co_l * pitch, *t1 = t0 + CN_BN * pitch;
-                float *srow = S + co_l * NP;
-                // all loads, then all stores (S and T share the array: one
-                // chain per element would serialise on the smem latency)
-                float v[8];
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
+            // repack into the dense box D[64][NP] (float4 along pixels: both
+            // sides conflict-free; loads batched before stores), then one
+            // TMA tensor store of the whole tile
+            float *D = S + ((CN_BN * SP + 255) & ~255);
+            const int q4 = NP / 4;
+            const int tid = threadIdx.x - 64;
+            for (int e0 = tid; e0 < CN_BN * q4; e0 += 4 * CN_EPI_WARPS * 32) {
+                float4 x[4];
 #pragma unroll
-                for (int j = 0; j < 8; j++) {
-                    const int pix = lane + 32 * j;
-                    v[j] = pix < NP ? t0[pix] + t1[pix] : 0.0f;
-                }
-#pragma unroll
-                for (int j = 0; j < 8; j++) {
-                    const int pix = lane + 32 * j;
-                    if (pix < NP) {
-                        if (p.epi.n)
-                            v[j] = apply_epilogue(p.epi, v[j], n, c0 + co_l, h0 + pix / p.tile_w, w0 + pix % p.tile_w);
-                        srow[pix] = v[j];
+                for (int u = 0; u < 4; u++) {
+                    const int e = e0 + u * CN_EPI_WARPS * 32;
+                    if (e < CN_BN * q4) {
+                        const int co_l = e / q4, px = (e - co_l * q4) * 4;
+                        x[u] = *reinterpret_cast<const float4 *>(S + co_l * SP + px);
                     }
                 }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int e = e0 + u * CN_EPI_WARPS * 32;
+                    if (e < CN_BN * q4) reinterpret_cast<float4 *>(D)[e] = x[u];
+                }
             }
-            if (ew == 0 && lane == 0) CN_TRACE(2, 6);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
             if (ew == 0 && lane == 0) {
-                if (!(p.dbg & 1)) tma_store_4d(&map_o, S, w0, h0, (int)c0, n);
+                if (!(p.dbg & 1)) tma_store_4d(&map_o, D, w0, h0, (int)c0, n);
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             }
-        }
-        // (channel, output row) pairs; lanes along the row
-        for (int rw = ew; rw < ((p.dbg & 1) || p.tma_out ? 0 : CN_BN * p.tile_h); rw += CN_EPI_WARPS) {
-            const int co_l = rw / p.tile_h, h = rw % p.tile_h;
-            const int64_t co = c0 + co_l;
-            const int ho = h0 + h;
-            if (co >= p.CO || ho >= p.HO) continue;
-            float *orow = p.o + n * p.so[0] + co * p.so[1] + (int64_t)ho * p.so[2];
-            const float *t0 = T + co_l * pitch + h * p.tile_w, *t1 = t0 + CN_BN * pitch;
-            for (int w = lane; w < p.tile_w; w += 32) {
-                const int wo = w0 + w;
-                if (wo >= p.WO) break;
-                float v = t0[w] + t1[w];
-                if (p.epi.n) v = apply_epilogue(p.epi, v, n, co, ho, wo);
-                orow[(int64_t)wo * p.so[3]] = v;
+        } else {
+            // (channel, output row) pairs; lanes along the row
+            for (int rw = ew; rw < ((p.dbg & 1) ? 0 : CN_BN * p.tile_h); rw += CN_EPI_WARPS) {
+                const int co_l = rw / p.tile_h, h = rw % p.tile_h;
+                const int64_t co = c0 + co_l;
+                const int ho = h0 + h;
+                if (co >= p.CO || ho >= p.HO) continue;
+                float *orow = p.o + n * p.so[0] + co * p.so[1] + (int64_t)ho * p.so[2];
+                const float *srow = S + co_l * SP + h * p.tile_w;
+                for (int w = lane; w < p.tile_w; w += 32) {
+                    const int wo = w0 + w;
+                    if (wo >= p.WO) break;
+                    orow[(int64_t)wo * p.so[3]] = srow[w];
+                }
             }
         }
     }

@@ -115,6 +115,9 @@ struct FilterImgArgs {
     int64_t CO, K, Kp, C, Cp, S;
     int64_t sw[4];
     float *img;
+    // 0: rows 0-63 hi, 64-127 lo; 1: channel c's hi / lo rows at
+    // 32 (c / 16) + 2 (c % 16) and +1 (tf32x3_conv_nhwc_t_kernel)
+    int ilv_rows;
 };
 
 __device__ __forceinline__ void filter_image_body(const FilterImgArgs &f, int *any, int gen, int first, int step) {
@@ -138,9 +141,11 @@ __device__ __forceinline__ void filter_image_body(const FilterImgArgs &f, int *a
         const float l = tf32_lo(v, h);
         if (any != nullptr && !(fabsf(v) < __int_as_float(0x7f800000))) *any = gen;
         float *base = f.img + ((int64_t)(ct * nkb + kb) * 2) * (CT_BN * CT_BK);
-        const int off = n * 16 + (((kk >> 2) ^ ((n >> 1) & 3)) << 2) + (kk & 3);   // floats
-        base[off] = h;
-        base[CT_BN * CT_BK + off] = l;
+        // row R of the 128-row K-major SW64 image: 16 floats, 16-B chunks XOR (R >> 1) & 3
+        const int rh = f.ilv_rows ? 32 * (n >> 4) + 2 * (n & 15) : n;
+        const int rl = f.ilv_rows ? rh + 1 : CT_BN + n;
+        base[rh * 16 + (((kk >> 2) ^ ((rh >> 1) & 3)) << 2) + (kk & 3)] = h;
+        base[rl * 16 + (((kk >> 2) ^ ((rl >> 1) & 3)) << 2) + (kk & 3)] = l;
     }
 }
 
