@@ -460,6 +460,9 @@ def run_gpu(args):
                 if any("tf32x3" in s for s in r["steps"]) and pk.get("bf16_tflops_sustained"):
                     ceil = pk["bf16_tflops_sustained"] / 6.0
                     per_config[other]["frac_tf32x3_ceiling"] = round(g / 1e3 / ceil, 4)
+                    if pk.get("bf16_tflops"):
+                        # a sub-ms step runs at burst clocks: the tighter bound
+                        per_config[other]["frac_tf32x3_burst_ceiling"] = round(g / 1e3 / (pk["bf16_tflops"] / 6.0), 4)
             except Exception as e:  # report, never hide
                 per_config[other] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0 and world == 1 and not args.no_cpu:
