@@ -26,6 +26,10 @@
  *     (program.py:182-183) so plans carry them verbatim.
  *   - thread-compatible, not thread-safe per stream (like the reference's
  *     CompiledKernel).
+ *   - library workspaces (split-K partials, the 3xTF32 split copies, the
+ *     max-plus fixup slots and flags) are per process and stream-ordered:
+ *     contractions enqueued on two different streams at once must not both
+ *     need them (run them on one stream, or synchronise in between).
  */
 #ifndef LSB_H_
 #define LSB_H_
