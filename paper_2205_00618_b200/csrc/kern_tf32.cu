@@ -211,13 +211,31 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
         snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
         return LSB_ERR_CUDA;
     }
+    // persistent launch (TcArgs::units): 128x256 GEMM tiles when there are
+    // more units than CTA slots; one CTA per SM (pairs: an even count)
+    constexpr bool kCanPersist = BN == 256 && Cf::kSmemBytesPersist <= 232448;
+    const int units = a.m_tiles * a.n_tiles + a.m_tiles2 * a.n_tiles2 + a.split_tiles;
+    int ctas = units;
+    a.units = 0;
+    if (kCanPersist && a.conv_hw == 0 && (a.fast_n || a.epi.n == 0) && !getenv("LSB_NO_PERSIST")) {
+        int slots = lsb::device_sms() * Cf::kCtasPerSm;
+        if (a.pair) slots &= ~1;
+        if (units > slots) {
+            a.units = units;
+            ctas = slots;
+        }
+    }
+    const size_t smem_bytes = a.units ? Cf::kSmemBytesPersist : Cf::kSmemBytes;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<BK, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<BK, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)Cf::kSmemBytes);
+        if constexpr (kCanPersist)
+            cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<BK, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Cf::kSmemBytesPersist);
         attr = true;
     }
-    dim3 grid((unsigned)(a.m_tiles * a.n_tiles + a.m_tiles2 * a.n_tiles2 + a.split_tiles));
+    dim3 grid((unsigned)ctas);
     static long long *trace = nullptr;
     const char *trace_path = getenv("LSB_GEMM_TRACE");
     if (trace_path) {
@@ -230,7 +248,7 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = grid;
         cfg.blockDim = dim3(Cf::kThreads);
-        cfg.dynamicSmemBytes = Cf::kSmemBytes;
+        cfg.dynamicSmemBytes = smem_bytes;
         cfg.stream = s;
         cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -241,7 +259,15 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
         attr[1].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 2;
-        cudaLaunchKernelEx(&cfg, tc::tf32x3_gemm_kernel<BK, BN>, mah, mal, mbh, mbl, a);
+        if constexpr (kCanPersist) {
+            if (a.units) {
+                cudaLaunchKernelEx(&cfg, tc::tf32x3_gemm_kernel<BK, BN, true>, mah, mal, mbh, mbl, a);
+            } else {
+                cudaLaunchKernelEx(&cfg, tc::tf32x3_gemm_kernel<BK, BN, false>, mah, mal, mbh, mbl, a);
+            }
+        } else {
+            cudaLaunchKernelEx(&cfg, tc::tf32x3_gemm_kernel<BK, BN, false>, mah, mal, mbh, mbl, a);
+        }
     }
     prof_mark(1, s);
     if (trace_path) {

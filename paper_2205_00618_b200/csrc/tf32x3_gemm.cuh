@@ -55,6 +55,10 @@ struct Cfg {
     static constexpr int kStageBytes = 2 * (kTileA + kTileB);
     static constexpr int kTmemCols = 2 * BN_;              // two chunk accumulators
     static constexpr size_t kSmemBytes = (size_t)STAGES * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    // persistent launches (TcArgs::units) stage the store through a 32x32
+    // float block per epilogue warp after the barriers: the stage ring is busy
+    // with the next unit's operands while a finished tile is stored
+    static constexpr size_t kSmemBytesPersist = kSmemBytes + (size_t)kEpiWarps * 32 * 32 * 4;
     static_assert(STAGES * kStageBytes >= BM * BN_ * 4, "epilogue staging reuses the stage buffers");
     static_assert(kTmemCols <= 512, "TMEM has 512 columns");
 };
@@ -105,6 +109,12 @@ struct TcArgs {
     // its chunk sum to split_ws; the second to arrive (split_cnt) adds the
     // other's, runs the epilogue and re-arms the counter.
     int split_tiles;
+    // persistent launch (units > 0, BN = 256 only): gridDim.x CTAs walk the
+    // units (tiles, then tail-split halves) t = blockIdx.x + i * gridDim.x.
+    // The TMA ring, the MMA issuer and the two TMEM chunk buffers run on
+    // across unit boundaries, so a finished tile's store (from registers,
+    // through a per-warp smem block) overlaps the next unit's first chunks.
+    int units;
     float *split_ws;
     int *split_cnt;
     const int *rowflag, *colflag, *anyflag;   // anyflag[0] A, [1] B
@@ -234,6 +244,22 @@ __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t 
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
+}
+
+// 32 lanes x 16 consecutive 32-bit columns -> 16 registers per thread (the
+// GEMM's chunk fold: 128 running sums + 16 leave room under the 168-register
+// cap of a 10-warp CTA)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; i++) v[i] = __uint_as_float(r[i]);
 }
 
 // 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread
@@ -525,7 +551,10 @@ __device__ void tc_nonfinite_fixup(const TcArgs &p) {
 
 // ---------------------------------------------------------------- main kernel
 
-template <int BK_, int BN_>
+// kPersist: the persistent instance (TcArgs::units > 0; no epilogue or the
+// fast one, GEMM only).  The single-unit instance keeps the staged store,
+// which inside a unit loop would not fit the register cap.
+template <int BK_, int BN_, bool kPersist>
 __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasPerSm)
     tf32x3_gemm_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                        const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
@@ -547,19 +576,27 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // grouped raster: consecutive CTAs walk kGroupM m-tiles before moving to
+    const int num_kb = (int)(p.Kp / BK);
+    const int all_chunks = (num_kb + kChunkStages - 1) / kChunkStages;
+    // unit t -> output tile, K half (-1: whole K) and split-tile slot.
+    // grouped raster: consecutive units walk kGroupM m-tiles before moving to
     // the next n-tile, so the CTAs resident together share A and B blocks
-    int mt, nt;
-    int half = -1, stile = 0;   // tail split: K half and split-tile slot
-    {
-        int t = blockIdx.x, mtiles = p.m_tiles, ntiles = p.n_tiles, mb = p.mt0, nb = p.nt0;
+    struct Unit {
+        int64_t m0, n0;
+        int half, stile, c_begin, num_chunks;
+    };
+    auto decode = [&](int t) {
+        Unit u;
+        int mtiles = p.m_tiles, ntiles = p.n_tiles, mb = p.mt0, nb = p.nt0;
+        u.half = -1;
+        u.stile = 0;
         if (p.split_tiles) {
             const int whole = p.m_tiles * p.n_tiles + p.m_tiles2 * p.n_tiles2 - p.split_tiles;
             if (t >= whole) {
-                const int u = t - whole;
-                stile = (u >> 2) * 2 + (u & 1);
-                half = (u >> 1) & 1;
-                t = whole + stile;
+                const int v = t - whole;
+                u.stile = (v >> 2) * 2 + (v & 1);
+                u.half = (v >> 1) & 1;
+                t = whole + u.stile;
             }
         }
         if (t >= p.m_tiles * p.n_tiles) {
@@ -570,15 +607,15 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
         const int g = t / per_group, first_m = g * kGroupM;
         const int gm = min(kGroupM, mtiles - first_m);
         const int r = t % per_group;
-        mt = mb + first_m + r % gm;
-        nt = nb + r / gm;
-    }
-    const int64_t m0 = (int64_t)mt * BM, n0 = (int64_t)nt * BN;
-    const int num_kb = (int)(p.Kp / BK);
-    const int all_chunks = (num_kb + kChunkStages - 1) / kChunkStages;
-    // this CTA's K chunks [c_begin, c_begin + num_chunks)
-    const int c_begin = half == 1 ? all_chunks / 2 : 0;
-    const int num_chunks = half < 0 ? all_chunks : half == 0 ? all_chunks / 2 : all_chunks - all_chunks / 2;
+        u.m0 = (int64_t)(mb + first_m + r % gm) * BM;
+        u.n0 = (int64_t)(nb + r / gm) * BN;
+        // this unit's K chunks [c_begin, c_begin + num_chunks)
+        u.c_begin = u.half == 1 ? all_chunks / 2 : 0;
+        u.num_chunks = u.half < 0 ? all_chunks : u.half == 0 ? all_chunks / 2 : all_chunks - all_chunks / 2;
+        return u;
+    };
+    const int units = kPersist ? p.units : (int)gridDim.x;
+    const int ustride = (int)gridDim.x;
     __shared__ int s_split_second;
     if (threadIdx.x == 0) TC_TRACE(3, 0);
 
@@ -617,8 +654,11 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
             asm volatile("griddepcontrol.wait;" ::: "memory");
             int stage = 0;
             uint32_t phase = 0;
-            const int kb_end = min(num_kb, (c_begin + num_chunks) * kChunkStages);
-            for (int kb = c_begin * kChunkStages; kb < kb_end; kb++) {
+            for (int t = blockIdx.x; t < units; t += ustride) {
+            const Unit u = decode(t);
+            const int64_t m0 = u.m0, n0 = u.n0;
+            const int kb_end = min(num_kb, (u.c_begin + u.num_chunks) * kChunkStages);
+            for (int kb = u.c_begin * kChunkStages; kb < kb_end; kb++) {
                 // paired release (even STAGES): a slot pair is freed by one
                 // commit after its second stage (see the MMA loop)
                 mbar_wait(&empty[kPairRelease ? (stage | 1) : stage], phase ^ 1);
@@ -643,6 +683,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                     phase ^= 1;
                 }
             }
+            }   // units
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (one thread)
@@ -650,13 +691,16 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
             constexpr uint32_t idesc = idesc_tf32(BM, BN);
             int stage = 0;
             uint32_t phase = 0;
-            for (int c = 0; c < num_chunks; c++) {
-                const int b = c & 1;
-                const uint32_t tphase = (uint32_t)((c >> 1) & 1);
+            uint32_t gc = 0;   // chunks issued so far (TMEM buffer, phase)
+            for (int t = blockIdx.x; t < units; t += ustride) {
+            const Unit u = decode(t);
+            for (int c = 0; c < u.num_chunks; c++, gc++) {
+                const int b = gc & 1;
+                const uint32_t tphase = (gc >> 1) & 1;
                 mbar_wait(&tempty[b], tphase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(b * BN);
-                const int kb_first = (c_begin + c) * kChunkStages;
+                const int kb_first = (u.c_begin + c) * kChunkStages;
                 const int kb_end = min(num_kb, kb_first + kChunkStages);
                 TC_TRACE(2, c);
                 for (int kb = kb_first; kb < kb_end; kb++) {
@@ -698,6 +742,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 }
                 umma_commit(&tfull[b]);           // chunk accumulator complete
             }
+            }   // units
         }
     } else {
         // ---------------- epilogue warps: warp w reads TMEM lane quadrant
@@ -705,25 +750,33 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
         const int q = warp & 3;
         const int ch = (warp - 2) >> 2;           // 128-column half of the tile
         const int row = q * 32 + lane;
+        uint32_t gc = 0;   // chunks folded so far (TMEM buffer, phase)
+        for (int t = blockIdx.x; t < units; t += ustride) {
         float tot[128];
 #pragma unroll
         for (int i = 0; i < 128; i++) tot[i] = 0.0f;
-        for (int c = 0; c < num_chunks; c++) {
-            const int b = c & 1;
-            mbar_wait(&tfull[b], (uint32_t)((c >> 1) & 1));
+        // only the chunk count is live across the fold (128 sums + 16 loaded
+        // columns sit at the 168-register cap); the rest is decoded after it
+        const int nch = decode(t).num_chunks;
+        for (int c = 0; c < nch; c++, gc++) {
+            const int b = gc & 1;
+            mbar_wait(&tfull[b], (gc >> 1) & 1);
             if (warp == 2 && lane == 0) TC_TRACE(1, c);
             tc_fence_after();
 #pragma unroll
-            for (int part = 0; part < 4; part++) {
-                float v[32];
-                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + ch * 128 + part * 32), v);
+            for (int part = 0; part < 8; part++) {
+                float v[16];
+                tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + ch * 128 + part * 16), v);
 #pragma unroll
-                for (int i = 0; i < 32; i++) tot[part * 32 + i] += v[i];
+                for (int i = 0; i < 16; i++) tot[part * 16 + i] += v[i];
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[b]);
         }
+        const Unit u = decode(t);
+        const int64_t m0 = u.m0, n0 = u.n0;
+        const int half = u.half, stile = u.stile;
         bool store = true;
         if (half >= 0) {
             // tail split: publish this half's sums (thread-major float4s, a
@@ -755,7 +808,60 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 if (et == 0) p.split_cnt[stile] = 0;   // re-armed for the next launch
             }
         }
+        if constexpr (kPersist) {
         if (store) {
+            // persistent: the stage ring already holds the next unit's
+            // operands.  Per 32-column block: the warp writes its 32 rows x 32
+            // columns to its own smem block (16-B chunks XOR-swizzled by row,
+            // conflict-free both ways), then stores 4 rows x 128 B per
+            // instruction with the epilogue applied
+            float *blk = reinterpret_cast<float *>(smem + STAGES * kStageBytes + 256) + (warp - 2) * 32 * 32;
+            const int sub = lane >> 3, cc = lane & 7;
+#pragma unroll
+            for (int bj = 0; bj < 4; bj++) {   // unrolled: tot[] stays in registers
+#pragma unroll
+                for (int c = 0; c < 8; c++)
+                    *reinterpret_cast<float4 *>(blk + lane * 32 + ((c ^ (lane & 7)) * 4)) =
+                        make_float4(tot[bj * 32 + c * 4], tot[bj * 32 + c * 4 + 1], tot[bj * 32 + c * 4 + 2],
+                                    tot[bj * 32 + c * 4 + 3]);
+                __syncwarp();
+                const int64_t n = n0 + ch * 128 + bj * 32 + cc * 4;
+                // host: persistent launches carry no epilogue or the fast one
+                float fb[2][4];
+#pragma unroll
+                for (int i = 0; i < 2; i++)
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        fb[i][e] = (i < p.fast_n && p.fbias[i] && n + e < p.N) ? __ldg(p.fbias[i] + (n + e) * p.fbias_stride[i]) : 0.f;
+#pragma unroll 2
+                for (int i = 0; i < 8; i++) {
+                    const int r = i * 4 + sub;
+                    const int64_t m = m0 + q * 32 + r;
+                    const float4 v = *reinterpret_cast<const float4 *>(blk + r * 32 + ((cc ^ (r & 7)) * 4));
+                    if (m >= p.M || n >= p.N) continue;
+                    float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int j = 0; j < 2; j++) {
+                        if (j >= p.fast_n) break;
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            if (p.fbias[j]) x[e] += fb[j][e];
+                            if (p.frelu[j]) x[e] = fmax_nan(x[e], 0.0f);
+                        }
+                    }
+                    float *dst = p.C + m * p.sc_m;
+                    if (p.c_vec && n + 3 < p.N) {
+                        *reinterpret_cast<float4 *>(dst + n) = make_float4(x[0], x[1], x[2], x[3]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; e++)
+                            if (n + e < p.N) dst[(n + e) * p.sc_n] = x[e];
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        } else if (store) {
         // stage the tile in (now idle) pipeline smem: row-major, 16-B chunks
         // XOR-swizzled by row so both the write and the read are conflict-free
         float *tile = reinterpret_cast<float *>(smem);
@@ -885,6 +991,8 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
             }
         }
         }   // store
+        if constexpr (!kPersist) break;   // one unit per CTA
+        }   // units
     }
     if (warp == 2 && lane == 0) TC_TRACE(3, 3);
     tc_fence_before();

@@ -1,0 +1,54 @@
+"""Persistent 3xTF32 GEMM launch (TcArgs::units, the 128x256 tile geometry
+when there are more units than SMs): ragged edges, the K-half tail split
+(units = whole tiles + split halves walked by 148 CTAs) and the bias+ReLU fast
+epilogue stored from registers, against the f64 oracle (integer inputs keep
+3xTF32 exact) and bit-for-bit against the one-unit-per-CTA launch."""
+import json
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from test_gpu_edges import _graph, _inputs, _run, _same
+
+pytestmark = pytest.mark.gpu
+
+# (m, k, n): 4096x4096 = 512 tiles -> 444 whole + 68 split tiles (C4's layout);
+# ragged m/n with partial last tiles; one K chunk (no split: chunks < 2)
+SHAPES = [(4096, 200, 4096), (1000, 300, 4100), (2050, 70, 3000), (1536, 64, 6144)]
+
+
+@pytest.mark.parametrize("m,k,n", SHAPES, ids=lambda v: str(v))
+def test_persistent_gemm_matches_oracle_and_single_unit(m, k, n, monkeypatch):
+    monkeypatch.setenv("LSB_GEMM_ALGO", "tf32x3")
+    monkeypatch.setenv("LSB_TC_CFG", "16x256")
+    gj = _graph("semiring_mul_add", m=m, k=k, n=n)
+    kern, ins = _inputs(gj, m * 131 + k * 7 + n)
+    got = _run(kern, ins)
+    out = next(s for s in got if s not in ins)
+    mvar = [v["id"] for v in json.loads(gj)["vars"] if v["name"] == "m"][0]
+    rows = np.unique(np.array([0, 127, 128, m // 2, m - 129, m - 1]).clip(0, m - 1))
+    ref = O.reference_eval(gj, ins, restrict={mvar: rows})
+    _same(got[out].reshape(m, n)[rows], ref[next(iter(ref))], exact=True)
+    monkeypatch.setenv("LSB_NO_PERSIST", "1")
+    single = _run(kern, ins)
+    assert np.array_equal(got[out].view(np.uint32), single[out].view(np.uint32))
+
+
+def test_persistent_fused_bias_relu(monkeypatch):
+    """The bias + ReLU pipeline (C4's, fused into the epilogue) at C4's tile
+    count through the persistent register store: exact against the oracle and
+    bit-for-bit equal to the staged single-unit store."""
+    monkeypatch.setenv("LSB_GEMM_ALGO", "tf32x3")
+    m, k, n = 4096, 96, 4096
+    gj = _graph("mlp_bias_relu_small", m=m, k=k, n=n)
+    kern, ins = _inputs(gj, 44)
+    got = _run(kern, ins)
+    mvar = [v["id"] for v in json.loads(gj)["vars"] if v["name"] == "m"][0]
+    rows = np.array([0, 1, 129, 2047, 4095])
+    ref = O.reference_eval(gj, ins, restrict={mvar: rows})
+    out = next(iter(ref))
+    _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
+    monkeypatch.setenv("LSB_NO_PERSIST", "1")
+    single = _run(kern, ins)
+    assert np.array_equal(got[out].view(np.uint32), single[out].view(np.uint32))
