@@ -40,15 +40,18 @@ def test_persistent_fused_bias_relu(monkeypatch):
     count through the persistent register store: exact against the oracle and
     bit-for-bit equal to the staged single-unit store."""
     monkeypatch.setenv("LSB_GEMM_ALGO", "tf32x3")
-    m, k, n = 4096, 96, 4096
-    gj = _graph("mlp_bias_relu_small", m=m, k=k, n=n)
+    monkeypatch.setenv("LSB_TC_CFG", "16x256")
+    import os
+    m, n = 4096, 4096
+    with open(os.path.join(os.path.dirname(__file__), "golden", "graphs", "C4.json")) as f:
+        gj = f.read()
     kern, ins = _inputs(gj, 44)
     got = _run(kern, ins)
-    mvar = [v["id"] for v in json.loads(gj)["vars"] if v["name"] == "m"][0]
     rows = np.array([0, 1, 129, 2047, 4095])
-    ref = O.reference_eval(gj, ins, restrict={mvar: rows})
-    out = next(iter(ref))
-    _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
+    out = [s for s in got if s not in ins][-1]
+    x, w, b = (ins[s] for s in sorted(ins))
+    ref = np.maximum(x[rows].astype(np.float64) @ w.astype(np.float64) + b.reshape(1, -1), 0.0)
+    _same(got[out].reshape(m, n)[rows], ref, exact=True)
     monkeypatch.setenv("LSB_NO_PERSIST", "1")
     single = _run(kern, ins)
     assert np.array_equal(got[out].view(np.uint32), single[out].view(np.uint32))
