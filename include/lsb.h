@@ -192,6 +192,11 @@ typedef struct {
 
 /* ---- lifecycle / errors --------------------------------------------------- */
 int lsb_abi_version(void);
+/* Binds the process to `device` (cudaSetDevice) and checks it is sm_100.
+ * One device per process: a second lsb_init with another device fails with
+ * LSB_ERR_UNSUPPORTED, and the compute calls fail unless the caller's
+ * current device is the bound one (workspaces and kernel attributes are
+ * process-wide; the multi-GPU path runs one process per GPU). */
 int lsb_init(int device);
 int lsb_last_error(char *buf, size_t len);
 int lsb_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,

@@ -47,6 +47,18 @@ int check_launch(const char *what) {
 
 int g_sm_count = 0;
 int sm_count();
+std::atomic<int> g_device{-1};   // the device lsb_init bound this process to
+
+// compute entry points run on the bound device only (the caller's current
+// device must be it)
+int check_device() {
+    const int bound = g_device.load(std::memory_order_relaxed);
+    if (bound < 0) return fail(LSB_ERR_INVALID, "lsb_init was not called");
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != bound)
+        return fail(LSB_ERR_UNSUPPORTED, "current device %d is not the device %d liblsb is bound to", cur, bound);
+    return LSB_OK;
+}
 
 }  // namespace
 
@@ -223,6 +235,12 @@ int lsb_init(int device) {
     int n = 0;
     LSB_CUDA(cudaGetDeviceCount(&n));
     if (device < 0 || device >= n) return fail(LSB_ERR_INVALID, "device %d of %d", device, n);
+    // one device per process: the workspaces, tensor-map entry point and
+    // kernel smem attributes are process-wide (one process per GPU)
+    int bound = -1;
+    if (!g_device.compare_exchange_strong(bound, device) && bound != device)
+        return fail(LSB_ERR_UNSUPPORTED, "liblsb is bound to device %d in this process; device %d needs its own process",
+                    bound, device);
     LSB_CUDA(cudaSetDevice(device));
     int major = 0;
     LSB_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
@@ -360,6 +378,7 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     int rc = check_epi(d->n_epi, d->epi);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
+    if ((rc = check_device())) return rc;
 
     if (d->flags & (LSB_GEMM_PREP_A | LSB_GEMM_PREP_B | LSB_GEMM_PRESPLIT)) {
         // blocked 3xTF32 sequence step: global coordinates throughout
@@ -588,6 +607,7 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     const int64_t K = d->C * d->R * d->S;
     if (K > lsb::kConvTableMax) return fail(LSB_ERR_UNSUPPORTED, "conv K=%lld too large", (long long)K);
     if (d->N > 65535) return fail(LSB_ERR_UNSUPPORTED, "too many images");
+    if ((rc = check_device())) return rc;
 
     lsb::ConvArgs a;
     memset(&a, 0, sizeof(a));
@@ -705,6 +725,7 @@ int lsb_affine_nest(const lsb_nest_desc *d, void *stream) {
     }
     a.out = d->out; a.out_addr = d->out_addr; a.beta = d->beta;
     a.epi = pack_epi(d->n_epi, d->epi);
+    if ((rc = check_device())) return rc;
     kNest[d->combine][d->reduce](a, (cudaStream_t)stream);
     return check_launch("affine_nest");
 }

@@ -34,9 +34,51 @@ def test_reference_arm_json_line():
 def test_reference_arm_nonzero_rank_is_silent():
     e = {"RANK": "1", "WORLD_SIZE": "2"}
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "C1",
-                          "--steps", "1", "--warmup", "0", "--ref-budget", "0.1"],
+                          "--gpus", "2", "--steps", "1", "--warmup", "0", "--ref-budget", "0.1"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT, env={**os.environ, **e})
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def _clean_env():
+    return {k: v for k, v in os.environ.items()
+            if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+
+
+def test_launcher_spawns_ranks_one_json_line():
+    """--gpus 2 without WORLD_SIZE: bench.py re-runs itself as 2 ranks under
+    torch.distributed.run; rank 0 alone prints, n_gpus is 2."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--config", "C1", "--steps", "1", "--warmup", "0", "--ref-budget", "0.1", "--no-vm"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=_clean_env())
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+
+
+def test_world_size_must_match_gpus():
+    e = {**_clean_env(), "RANK": "0", "WORLD_SIZE": "2", "LOCAL_RANK": "0"}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "4",
+                          "--config", "C1", "--steps", "1", "--no-vm"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=e)
+    assert out.returncode == 2 and "WORLD_SIZE" in out.stderr
+
+
+@pytest.mark.gpu
+def test_bench_c5_through_launcher():
+    """The headline config through the torchrun launcher path (1 rank): one
+    JSON line, n_gpus 1, the shard's sampled rows pass the f64 check."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--launch",
+                          "--config", "C5", "--steps", "3", "--warmup", "3", "--no-per-config", "--no-cpu"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=_clean_env())
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["parity"]["ok"] and d["parity"]["ref_metric"] <= 1e-4, d["parity"]
+    assert d["clocks"]["sm_mhz"], d["clocks"]
 
 
 @pytest.mark.gpu

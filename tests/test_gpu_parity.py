@@ -14,6 +14,8 @@ through the C ABI in liblsb.so.  Rules (BASELINE north_star):
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -153,6 +155,8 @@ def test_c2_maxplus_bit_exact_vs_reference_vm():
 
 @pytest.mark.parametrize("name", ["C3", "C3g"])
 def test_c3_conv(name):
+    """All 8 images: image 0 against the stored reference_eval output, every
+    image against the oracle restatement (f64) restricted to that image."""
     cfg = common.config("C3")
     bufs = common.config_inputs(name)
     graph = common.graph_json(cfg["graph"] if name == "C3" else cfg["graph_guarded"])
@@ -162,17 +166,31 @@ def test_c3_conv(name):
     d = np.load(common.GOLDEN + "/" + cfg["data"])
     ref0 = d["ref_img0"].astype(np.float64).reshape(64, 56, 56)
     assert common.strict_ok(o[0], ref0).all()
-    # the other images: oracle restatement (f64) on image 7
     from oracle import oracle as O
     from paper_2205_00618_b200.graph import Graph
     g = Graph.from_json(graph)
     nvar = [v.id for v in g.vars.values() if v.name == "n"][0]
-    ref7 = O.reference_eval(g, bufs, restrict={nvar: np.array([7])})[2]
-    assert common.strict_ok(o[7:8], ref7).all()
+    for img in range(8):
+        ref = O.reference_eval(g, bufs, restrict={nvar: np.array([img])})[2]
+        ok = common.strict_ok(o[img:img + 1], ref)
+        assert ok.all(), (img, float(ok.mean()), common.ref_metric(o[img:img + 1], ref))
+
+
+def _f64_gemm_rows(X, W, b=None, relu=False, block=512):
+    out = np.empty((X.shape[0], W.shape[1]), np.float64)
+    W64 = W.astype(np.float64)
+    for r in range(0, X.shape[0], block):
+        y = X[r:r + block].astype(np.float64) @ W64
+        if b is not None:
+            y += b.astype(np.float64)
+        out[r:r + block] = np.maximum(y, 0.0) if relu else y
+    return out
 
 
 @pytest.mark.parametrize("bias_nonzero", [False, True])
 def test_c4_mlp_bias_relu(bias_nonzero):
+    """All 4096 x 4096 outputs against an f64 restatement (rows 0-63 also
+    against the stored reference_eval output)."""
     cfg = common.config("C4")
     bufs = common.config_inputs("C4", bias_nonzero)
     k, got = _run(common.graph_json(cfg["graph"]), bufs)
@@ -181,11 +199,9 @@ def test_c4_mlp_bias_relu(bias_nonzero):
     d = np.load(common.GOLDEN + "/" + cfg["data"])
     ref = d["ref_rows0_64_bnz" if bias_nonzero else "ref_rows0_64_b0"]
     assert common.strict_ok(y[:64], ref).all()
-    # sampled rows across the whole output, f64 restatement
-    rows = np.array([100, 1999, 4095])
-    X, W, b = (bufs[i].astype(np.float64) for i in range(3))
-    want = np.maximum(X[rows] @ W + b, 0.0)
-    assert common.strict_ok(y[rows], want).all()
+    want = _f64_gemm_rows(bufs[0], bufs[1], bufs[2], relu=True)
+    ok = common.strict_ok(y, want)
+    assert ok.all(), (float(ok.mean()), common.ref_metric(y, want))
 
 
 def test_c4_alpha_form():
@@ -198,23 +214,46 @@ def test_c4_alpha_form():
 
 
 @pytest.mark.slow
-def test_c5_gemm_16384_sampled():
+def test_c5_gemm_16384_full():
+    """Every one of the 16384^2 outputs against an f64 GEMM (computed on the
+    device in torch float64 -- the f64 restatement of reference_eval's
+    (mul, add) contraction).  Gate: the reference metric
+    max|d|/max(|ref|,1) <= 1e-4; the strict per-element pass fraction is
+    recorded next to the reference VM's own on rows 0-7 (the VM fails the
+    strict rule on ~0.6 % at K = 16384) and must not be worse than it."""
+    import json
+    import torch
     cfg = common.config("C5")
     bufs = common.config_inputs("C5")
     _, got = _run(common.graph_json(cfg["graph"]), bufs)
     C = got[2].reshape(16384, 16384)
     d = np.load(common.GOLDEN + "/" + cfg["data"])
     ref8 = d["ref_rows0_8"]
-    m = common.ref_metric(C[:8], ref8)
-    ours = float(common.strict_ok(C[:8], ref8).mean())
     vm = float(common.strict_ok(d["vm_rows0_8"], ref8).mean())
-    print(f"C5 rows0-8: metric {m:.2e}, strict pass {ours:.4f} (reference VM {vm:.4f})")
-    assert m <= 1e-4
-    rng = np.random.default_rng(7)
-    rows = np.sort(rng.choice(16384, 48, replace=False))
-    cols = np.sort(rng.choice(16384, 256, replace=False))
-    want = bufs[0][rows].astype(np.float64) @ bufs[1][:, cols].astype(np.float64)
-    assert common.ref_metric(C[np.ix_(rows, cols)], want) <= 1e-4
+    dev = torch.device("cuda", 0)
+    A = torch.from_numpy(bufs[0]).to(dev).double()
+    B = torch.from_numpy(bufs[1]).to(dev).double()
+    Cg = torch.from_numpy(C).to(dev)
+    worst, npass, amax, tot = 0.0, 0, 0.0, 0
+    for r in range(0, 16384, 2048):
+        ref = A[r:r + 2048] @ B
+        dd = (Cg[r:r + 2048].double() - ref).abs()
+        worst = max(worst, float(dd.max()))
+        amax = max(amax, float(ref.abs().max()))
+        npass += int((dd <= 1e-5 + 1e-4 * ref.abs()).sum())
+        tot += ref.numel()
+    metric = worst / max(amax, 1.0)
+    strict = npass / tot
+    rec = {"config": "C5", "elements": tot, "ref_metric": metric, "strict_pass": strict,
+           "vm_strict_pass_rows0_8": vm, "ours_strict_pass_rows0_8": float(common.strict_ok(C[:8], ref8).mean()),
+           "ours_ref_metric_rows0_8": common.ref_metric(C[:8], ref8)}
+    print("C5 parity:", json.dumps(rec))
+    out = os.environ.get("LSB_PARITY_OUT")
+    if out:
+        with open(out, "w") as f:
+            json.dump(rec, f, indent=1)
+    assert metric <= 1e-4
+    assert strict >= vm, rec
 
 
 def test_launch_accounting():
