@@ -199,6 +199,9 @@ int lsb_abi_version(void);
  * process-wide; the multi-GPU path runs one process per GPU). */
 int lsb_init(int device);
 int lsb_last_error(char *buf, size_t len);
+/* Re-read the LSB_* environment knobs.  The library reads
+ * them once, at first use; nothing on the launch path calls getenv. */
+int lsb_reload_env(void);
 int lsb_device_info(int device, int *sm_count, int *cc_major, int *cc_minor,
                     int *clock_khz);
 

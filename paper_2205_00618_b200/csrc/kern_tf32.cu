@@ -11,8 +11,7 @@
 #include <mutex>
 
 #include "lsb_dispatch.cuh"
-#include "tf32x3_conv.cuh"
-#include "tf32x3_conv_tma.cuh"
+#include "conv_planar.cuh"
 #include "tf32x3_conv_nhwc.cuh"
 #include "tf32x3_gemm.cuh"
 
@@ -127,14 +126,14 @@ void launch_split(const float *X, int64_t R, int64_t Kd, int64_t s_r, int64_t s_
                   int ilv, int *flag, int *any, int gen, cudaStream_t s) {
     const bool small = R * Kp < (1ll << 31) && R * std::max<int64_t>(s_r, 1) + Kd * std::max<int64_t>(s_k, 1) < (1ll << 31);
     const bool al = reinterpret_cast<uintptr_t>(X) % 16 == 0 && Kp % 4 == 0;
-    if (small && al && s_k == 1 && s_r % 4 == 0 && Kd % 4 == 0 && !getenv("LSB_SCALAR_SPLIT")) {
+    if (small && al && s_k == 1 && s_r % 4 == 0 && Kd % 4 == 0 && !knobs().scalar_split) {
         const int64_t units = R * (Kp / 4);
         const unsigned blocks = (unsigned)std::min<int64_t>((units + 255) / 256, 148 * 16);
         tc::tf32_split_kcontig_kernel<<<blocks, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_r, hi, lo, (int)Kp, ilv, flag,
                                                               any, gen);
         return;
     }
-    if (small && al && s_r == 1 && s_k % 4 == 0 && R % 4 == 0 && !getenv("LSB_SCALAR_SPLIT")) {
+    if (small && al && s_r == 1 && s_k % 4 == 0 && R % 4 == 0 && !knobs().scalar_split) {
         dim3 g((unsigned)((Kp + 31) / 32), (unsigned)((R + 31) / 32));
         tc::tf32_split_rcontig_kernel<<<g, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_k, hi, lo, (int)Kp, ilv, flag, any,
                                                               gen);
@@ -184,12 +183,12 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
     a.bn = BN;
     // 2-CTA clusters over m-tile pairs (the raster keeps pairs on one n-tile
     // when m_tiles is even): B's half tiles are multicast (TcArgs::pair)
-    a.pair = (a.ilv && a.conv_hw == 0 && a.m_tiles % 2 == 0 && a.m_tiles2 % 2 == 0 && !getenv("LSB_NO_PAIR")) ? 1 : 0;
+    a.pair = (a.ilv && a.m_tiles % 2 == 0 && a.m_tiles2 % 2 == 0 && !knobs().no_pair) ? 1 : 0;
     // tail split: a last wave at most half full runs as twice the CTAs over
     // half the K chunks each (C4: 512 tiles = 3 waves + 68 -> 444 + 136 halves).
     // Whole-output GEMM launches only (blocked rectangles keep one order).
     a.split_tiles = 0;
-    if (whole && a.conv_hw == 0 && !getenv("LSB_NO_TAIL_SPLIT")) {
+    if (whole && !knobs().no_tail_split) {
         const int T = a.m_tiles * a.n_tiles;
         const int slots = lsb::device_sms() * Cf::kCtasPerSm;
         const int rem = T % slots;
@@ -217,7 +216,7 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
     const int units = a.m_tiles * a.n_tiles + a.m_tiles2 * a.n_tiles2 + a.split_tiles;
     int ctas = units;
     a.units = 0;
-    if (kCanPersist && a.conv_hw == 0 && (a.fast_n || a.epi.n == 0) && !getenv("LSB_NO_PERSIST")) {
+    if (kCanPersist && (a.fast_n || a.epi.n == 0) && !knobs().no_persist) {
         int slots = lsb::device_sms() * Cf::kCtasPerSm;
         if (a.pair) slots &= ~1;
         if (units > slots) {
@@ -237,7 +236,7 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
     }
     dim3 grid((unsigned)ctas);
     static long long *trace = nullptr;
-    const char *trace_path = getenv("LSB_GEMM_TRACE");
+    const char *trace_path = knobs().gemm_trace[0] ? knobs().gemm_trace : nullptr;
     if (trace_path) {
         if (!trace) cudaMalloc(&trace, 4 * 128 * sizeof(long long));
         cudaMemsetAsync(trace, 0, 4 * 128 * sizeof(long long), s);
@@ -296,11 +295,7 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
 int pick_cfg(int64_t N, int64_t K, bool has_epi) {
     (void)K;
     (void)has_epi;
-    if (const char *e = getenv("LSB_TC_CFG")) {
-        if (!strcmp(e, "16x128")) return 0;
-        if (!strcmp(e, "32x128")) return 1;
-        if (!strcmp(e, "16x256")) return 2;
-    }
+    if (knobs().tc_cfg >= 0) return knobs().tc_cfg;
     return N >= 256 ? 2 : 0;
 }
 
@@ -320,7 +315,7 @@ bool tf32x3_supported(int64_t M, int64_t N, int64_t K) {
 // fast epilogue when every stage is "(+ row-invariant operand[n]) then
 // identity|ReLU" with beta 1 and no C_in (C4's bias + ReLU)
 void set_fast_epilogue(tc::TcArgs &a, const EpiStages &epi) {
-    if (epi.n >= 1 && epi.n <= 2 && !getenv("LSB_NO_FAST_EPI")) {
+    if (epi.n >= 1 && epi.n <= 2 && !knobs().no_fast_epi) {
         bool ok = true;
         for (int i = 0; i < epi.n && ok; i++) {
             const lsb_epi_stage &st = epi.s[i];
@@ -352,7 +347,7 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     const int64_t Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
     const size_t need = sizeof(float) * (size_t)(2 * M + 2 * N) * (size_t)Kp;
     const int cfg = pick_cfg(N, K, epi.n > 0);
-    const int ilv = (cfg != 1 && !getenv("LSB_NO_ILV")) ? 1 : 0;   // BK = 16 tiles read [hi16 | lo16] rows
+    const int ilv = (cfg != 1 && !knobs().no_ilv) ? 1 : 0;   // BK = 16 tiles read [hi16 | lo16] rows
     float *ws;
     bool reuse_b = false;
     {
@@ -418,253 +413,6 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     return run_main_cfg(cfg, ahi, alo, bhi, blo, M, N, Kp, a, s, err, errlen);
 }
 
-// NCHW conv on the tensor cores: im2col+split prepass of the input (B, one
-// row per output pixel), gather+split of the filters (A, one row per output
-// channel), then the same 3xTF32 kernel in conv-output mode (m = co, n = pixel).
-int tf32x3_conv(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen) {
-    if (!load_encode()) {
-        snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
-        return LSB_ERR_UNSUPPORTED;
-    }
-    const int64_t M = c.M, K = c.K, P = n_img * c.N;   // c.N = HO*WO pixels per image
-    const int64_t Kp = (K + 31) / 32 * 32;
-    const size_t need = sizeof(float) * (size_t)(2 * M + 2 * P) * (size_t)Kp;
-    float *ws;
-    {
-        std::lock_guard<std::mutex> lk(g_tc_mu);
-        if (need > g_split_bytes) {
-            if (g_split) {
-                cudaDeviceSynchronize();
-                cudaFree(g_split);
-                g_split = nullptr;
-                g_split_bytes = 0;
-            }
-            if (cudaMalloc(&g_split, need) != cudaSuccess) {
-                snprintf(err, errlen, "cudaMalloc(%zu) for the tf32 conv operands failed", need);
-                return LSB_ERR_NOMEM;
-            }
-            g_split_bytes = need;
-        }
-        g_bkey = BKey{};
-        ws = g_split;
-    }
-    float *bhi = ws, *blo = bhi + P * Kp, *ahi = blo + P * Kp, *alo = ahi + M * Kp;
-    tc::ConvGeom g;
-    g.C = c.C; g.H = c.H; g.W = c.W; g.R = c.R; g.S = c.S; g.HO = c.HO; g.WO = c.WO;
-    g.P = P; g.K = K; g.Kp = Kp;
-    g.sh = c.stride_h; g.sw = c.stride_w; g.ph = c.pad_h; g.pw = c.pad_w; g.dh = c.dil_h; g.dw = c.dil_w;
-    g.sx0 = c.sx0; g.sx1 = c.sx1; g.sx2 = c.sx2; g.sx3 = c.sx3;
-    g.fill = c.fill;
-    dim3 gi((unsigned)((Kp + 31) / 32), (unsigned)((P + 31) / 32));
-    tc::im2col_split_kernel<<<gi, 256, 0, s>>>(c.x, g, bhi, blo);
-    const int64_t wtot = M * Kp;
-    tc::filter_split_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
-        c.w, M, K, Kp, c.C, c.R, c.S, c.sw0, c.sw1, c.sw2, c.sw3, 0, ahi, alo);
-    if (aux_launches) *aux_launches = 2;
-    tc::TcArgs a;
-    memset(&a, 0, sizeof(a));
-    a.M = M; a.N = P; a.K = K; a.Kp = Kp;
-    a.C = c.o;
-    a.conv_hw = c.HO * c.WO; a.conv_wo = c.WO;
-    a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
-    a.epi = c.epi;
-    return run_main_cfg(0, ahi, alo, bhi, blo, M, P, Kp, a, s, err, errlen);
-}
-
-// the gather zero-fills out-of-range taps and indexes X with 32-bit offsets
-bool tf32x3_conv_direct_ok(const ConvArgs &c, int64_t n_img) {
-    if ((c.K + 31) / 32 * 32 > tc::CV_MAX_K || c.fill != 0.0f) return false;
-    const int64_t span = (n_img - 1) * std::llabs(c.sx0) + (c.C - 1) * std::llabs(c.sx1) +
-                         (c.H - 1) * std::llabs(c.sx2) + (c.W - 1) * std::llabs(c.sx3);
-    if (span >= ((int64_t)1 << 31) || c.sx0 < 0 || c.sx1 < 0 || c.sx2 < 0 || c.sx3 < 0) return false;
-    return load_encode();
-}
-
-// in-kernel im2col (tf32x3_conv.cuh): only the filters are pre-split
-int tf32x3_conv_direct(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err,
-                       size_t errlen) {
-    if (!tf32x3_conv_direct_ok(c, n_img)) {
-        snprintf(err, errlen, "direct tf32x3 conv needs C*R*S <= %d, a 0 fill and a < 2^31-element input",
-                 tc::CV_MAX_K);
-        return LSB_ERR_UNSUPPORTED;
-    }
-    const int64_t CO = c.M, K = c.K, P = n_img * c.N;
-    const int64_t Kp = (K + 31) / 32 * 32;
-    const size_t need = sizeof(float) * (size_t)(2 * CO) * (size_t)Kp;
-    float *ws;
-    {
-        std::lock_guard<std::mutex> lk(g_tc_mu);
-        if (need > g_split_bytes) {
-            if (g_split) {
-                cudaDeviceSynchronize();
-                cudaFree(g_split);
-                g_split = nullptr;
-                g_split_bytes = 0;
-            }
-            if (cudaMalloc(&g_split, need) != cudaSuccess) {
-                snprintf(err, errlen, "cudaMalloc(%zu) for the tf32 filters failed", need);
-                return LSB_ERR_NOMEM;
-            }
-            g_split_bytes = need;
-        }
-        g_bkey = BKey{};
-        ws = g_split;
-    }
-    float *whi = ws, *wlo = whi + CO * Kp;
-    const int64_t wtot = CO * Kp;
-    tc::filter_split_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(
-        c.w, CO, K, Kp, c.C, c.R, c.S, c.sw0, c.sw1, c.sw2, c.sw3, 0, whi, wlo);
-    if (aux_launches) *aux_launches = 1;
-    CUtensorMap mwh, mwl;
-    if (!make_map(&mwh, whi, CO, Kp, tc::CV_BK, tc::CV_BN) || !make_map(&mwl, wlo, CO, Kp, tc::CV_BK, tc::CV_BN)) {
-        snprintf(err, errlen, "cuTensorMapEncodeTiled failed");
-        return LSB_ERR_CUDA;
-    }
-    const bool row4 = c.WO % 4 == 0 && c.stride_w == 1 && c.sx3 == 1 && (c.S - 1) * c.dil_w + 3 <= 31;
-    auto kern = row4 ? tc::tf32x3_conv_kernel<true> : tc::tf32x3_conv_kernel<false>;
-    static bool attr[2] = {false, false};
-    if (!attr[row4]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::cv_smem_bytes(tc::CV_MAX_K));
-        attr[row4] = true;
-    }
-    tc::ConvTcArgs a;
-    memset(&a, 0, sizeof(a));
-    tc::ConvGeom &g = a.g;
-    g.C = c.C; g.H = c.H; g.W = c.W; g.R = c.R; g.S = c.S; g.HO = c.HO; g.WO = c.WO;
-    g.P = P; g.K = K; g.Kp = Kp;
-    g.sh = c.stride_h; g.sw = c.stride_w; g.ph = c.pad_h; g.pw = c.pad_w; g.dh = c.dil_h; g.dw = c.dil_w;
-    g.sx0 = c.sx0; g.sx1 = c.sx1; g.sx2 = c.sx2; g.sx3 = c.sx3;
-    g.fill = c.fill;
-    g.x = c.x;
-    a.CO = CO;
-    a.o = c.o;
-    a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
-    const int num_kb = (int)(Kp / tc::CV_BK);
-    a.stages_per_chunk = (num_kb + tc::CV_CHUNKS - 1) / tc::CV_CHUNKS;
-    a.epi = c.epi;
-    dim3 grid((unsigned)((P + tc::CV_BM - 1) / tc::CV_BM), (unsigned)((CO + tc::CV_BN - 1) / tc::CV_BN));
-    static long long *trace = nullptr;
-    const bool tracing = getenv("LSB_CONV_TRACE") != nullptr;
-    if (tracing) {
-        if (!trace) cudaMalloc(&trace, 11 * 64 * sizeof(long long));
-        cudaMemsetAsync(trace, 0, 11 * 64 * sizeof(long long), s);
-        a.trace = trace;
-    }
-    prof_mark(0, s);
-    kern<<<grid, tc::CV_THREADS, tc::cv_smem_bytes(Kp), s>>>(mwh, mwl, a);
-    prof_mark(1, s);
-    if (tracing) {
-        long long h[11 * 64];
-        cudaStreamSynchronize(s);
-        cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
-        FILE *f = fopen(getenv("LSB_CONV_TRACE"), "w");
-        if (f) {
-            for (int e = 0; e < 11; e++) {
-                for (int k = 0; k < 64; k++) fprintf(f, "%lld ", h[e * 64 + k]);
-                fprintf(f, "\n");
-            }
-            fclose(f);
-        }
-    }
-    return LSB_OK;
-}
-
-}  // namespace lsb
-
-namespace lsb {
-
-// TMA-fed conv (tf32x3_conv_tma.cuh): unit column stride, 4 | C, a 0 fill,
-// TMA-legal strides (16-B multiples, 16-B aligned base), row stride <= 8
-bool tf32x3_conv_tma_ok(const ConvArgs &c, int64_t n_img) {
-    const int64_t Kp = (c.K + 15) / 16 * 16;
-    if (c.stride_w != 1 || c.sx3 != 1 || c.C % 4 != 0 || c.fill != 0.0f || Kp / 4 > tc::CT_MAX_GROUPS) return false;
-    if (c.stride_h < 1 || c.stride_h > 8 || c.dil_w < 1 || c.dil_h < 1) return false;
-    if (c.sx0 % 4 || c.sx1 % 4 || c.sx2 % 4 || c.sx0 <= 0 || c.sx1 <= 0 || c.sx2 <= 0) return false;
-    if (reinterpret_cast<uintptr_t>(c.x) % 16) return false;
-    if (c.W > (1 << 30) || c.H > (1 << 30) || n_img > (1 << 30)) return false;
-    return load_encode();
-}
-
-int tf32x3_conv_tma(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen) {
-    if (!tf32x3_conv_tma_ok(c, n_img)) {
-        snprintf(err, errlen, "TMA conv needs stride_w 1, C %% 4 == 0, a 0 fill and 16-B strides");
-        return LSB_ERR_UNSUPPORTED;
-    }
-    const int64_t CO = c.M, K = c.K;
-    const int64_t Kp = (K + 15) / 16 * 16;
-    float *ws = acquire_ws(sizeof(float) * 2 * (size_t)((CO + tc::CT_BN - 1) / tc::CT_BN * tc::CT_BN) * (size_t)Kp,
-                           err, errlen);
-    if (!ws) return LSB_ERR_NOMEM;
-    const int64_t co_tiles = (CO + tc::CT_BN - 1) / tc::CT_BN;
-    const int64_t wtot = co_tiles * Kp * tc::CT_BN;
-    {
-        tc::FilterImgArgs f{c.w, CO, K, Kp, c.C, c.C, c.S, {c.sw0, c.sw1, c.sw2, c.sw3}, ws};
-        tc::filter_image_kernel<<<(unsigned)std::min<int64_t>((wtot + 255) / 256, 4096), 256, 0, s>>>(f, nullptr, 0);
-    }
-    if (aux_launches) *aux_launches = 1;
-    CUtensorMap mx;
-    {
-        // X as (W, C, H, N) with its own strides; box 36 x 4 x 4 rows (every
-        // stride_h-th row via the element stride), zero fill out of range
-        cuuint64_t dims[4] = {(cuuint64_t)c.W, (cuuint64_t)c.C, (cuuint64_t)c.H, (cuuint64_t)n_img};
-        cuuint64_t strides[3] = {(cuuint64_t)c.sx1 * 4, (cuuint64_t)c.sx2 * 4, (cuuint64_t)c.sx0 * 4};
-        cuuint32_t box[4] = {(cuuint32_t)tc::CT_RAW_W, 4, (cuuint32_t)(4 * c.stride_h), 1};
-        cuuint32_t estr[4] = {1, 1, (cuuint32_t)c.stride_h, 1};
-        CUresult r = g_encode(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(c.x), dims, strides, box,
-                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) {
-            snprintf(err, errlen, "cuTensorMapEncodeTiled failed (input, %d)", (int)r);
-            return LSB_ERR_CUDA;
-        }
-    }
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(tc::tf32x3_conv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tc::ct_smem_bytes(tc::CT_MAX_GROUPS));
-        attr = true;
-    }
-    tc::ConvTmaArgs a;
-    memset(&a, 0, sizeof(a));
-    a.C = c.C; a.K = K; a.Kp = Kp; a.R = c.R; a.S = c.S; a.HO = c.HO; a.WO = c.WO;
-    a.ph = c.pad_h; a.pw = c.pad_w; a.dh = c.dil_h; a.dw = c.dil_w; a.sh = c.stride_h;
-    a.n_img = n_img;
-    a.tiles_h = (c.HO + 3) / 4;
-    a.tiles_w = (c.WO + 31) / 32;
-    a.CO = CO;
-    a.wimg = ws;
-    if (const char *dbg = getenv("LSB_CT_DBG")) a.dbg = atoi(dbg);
-    a.o = c.o;
-    a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
-    const int num_kb = (int)(Kp / tc::CT_BK);
-    a.stages_per_chunk = (num_kb + tc::CT_CHUNKS - 1) / tc::CT_CHUNKS;
-    a.epi = c.epi;
-    dim3 grid((unsigned)(n_img * a.tiles_h * a.tiles_w), (unsigned)((CO + tc::CT_BN - 1) / tc::CT_BN));
-    static long long *trace = nullptr;
-    const char *trace_path = getenv("LSB_CONV_TRACE");
-    if (trace_path) {
-        if (!trace) cudaMalloc(&trace, 6 * 64 * sizeof(long long));
-        cudaMemsetAsync(trace, 0, 6 * 64 * sizeof(long long), s);
-        a.trace = trace;
-    }
-    prof_mark(0, s);
-    tc::tf32x3_conv_tma_kernel<<<grid, tc::CT_THREADS, tc::ct_smem_bytes(Kp / 4), s>>>(mx, a);
-    prof_mark(1, s);
-    if (trace_path) {
-        long long h[6 * 64];
-        cudaStreamSynchronize(s);
-        cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
-        if (FILE *f = fopen(trace_path, "w")) {
-            for (int e = 0; e < 6; e++) {
-                for (int k = 0; k < 64; k++) fprintf(f, "%lld ", h[e * 64 + k]);
-                fprintf(f, "\n");
-            }
-            fclose(f);
-        }
-    }
-    return LSB_OK;
-}
-
 }  // namespace lsb
 
 namespace lsb {
@@ -706,30 +454,6 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
         gen = ++g_gen;
         if (gen <= 0) gen = g_gen = 1;
     }
-    // channel-major variant (tf32x3_conv_nhwc_t_kernel): tile_w x tile_h
-    // pixels on the MMA's N (<= 256, a multiple of 16); LSB_CONV_VARIANT=p|t
-    int tw_t = 0, th_t = 0, st_t = 0, sb_t = 0;
-    {
-        const char *cv = getenv("LSB_CONV_VARIANT");
-        bool want = cv ? !strcmp(cv, "t") : false;
-        if (want) {
-            int tw = (int)std::min<int64_t>((c.WO + 7) / 8 * 8, 256 / c.stride_w / 8 * 8);
-            int th = tw > 0 ? (int)std::min<int64_t>({256 / tw, 256 / c.stride_h, c.HO}) : 0;
-            if (const char *e = getenv("LSB_CONV_TW")) tw = atoi(e);   // experiments
-            if (const char *e = getenv("LSB_CONV_TH")) th = atoi(e);
-            while (th > 0 && (tw * th) % 16) th--;
-            const int np = tw * th;
-            if (np >= 64) {
-                const int sb = np * 128 + tc::CN_TILE_B;
-                int st = std::min(tc::CT_MAX_STAGES, (227 * 1024 - 1024 - 256) / sb) & ~1;
-                // epilogue staging: S[64][np + 8], then the dense box D[64][np]
-                const int64_t stage_need = ((int64_t)64 * (np + 8) + 255) / 256 * 256 * 4 + (int64_t)64 * np * 4;
-                if (st >= 2 && stage_need <= (int64_t)st * sb) {
-                    tw_t = tw; th_t = th; st_t = st; sb_t = sb;
-                }
-            }
-        }
-    }
     {
         dim3 g((unsigned)((c.W + 31) / 32), (unsigned)((Cp + 31) / 32), (unsigned)(n_img * c.H));
         const bool vec = c.sx3 == 1 && c.W % 4 == 0 && c.sx0 % 4 == 0 && c.sx1 % 4 == 0 && c.sx2 % 4 == 0 &&
@@ -737,7 +461,7 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
                          (n_img - 1) * c.sx0 + (c.C - 1) * c.sx1 + (c.H - 1) * c.sx2 + c.W < (1ll << 31) &&
                          (int64_t)xel < (1ll << 31);
         const int64_t wtot = co_tiles * tc::CN_BN * K;
-        tc::FilterImgArgs f{c.w, CO, K, K, c.C, Cp, c.S, {c.sw0, c.sw1, c.sw2, c.sw3}, wimg, tw_t ? 1 : 0};
+        tc::FilterImgArgs f{c.w, CO, K, K, c.C, Cp, c.S, {c.sw0, c.sw1, c.sw2, c.sw3}, wimg, 0};
         if (vec) {
             // one launch: X split blocks, then ceil(filter blocks / (gx*gy)) z-slices of filter work
             const unsigned zsplit = (unsigned)(n_img * ((c.H + tc::kSplitRows - 1) / tc::kSplitRows));
@@ -764,8 +488,7 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
         cuuint64_t dims[5] = {32, (cuuint64_t)cbn, (cuuint64_t)c.W, (cuuint64_t)c.H, (cuuint64_t)n_img};
         cuuint64_t strides[4] = {128, (cuuint64_t)cbn * 128, (cuuint64_t)(c.W * cbn) * 128,
                                  (cuuint64_t)(c.H * c.W * cbn) * 128};
-        cuuint32_t box[5] = {32, 1, (cuuint32_t)((tw_t ? tw_t : 32) * c.stride_w),
-                             (cuuint32_t)((th_t ? th_t : 4) * c.stride_h), 1};
+        cuuint32_t box[5] = {32, 1, (cuuint32_t)(32 * c.stride_w), (cuuint32_t)(4 * c.stride_h), 1};
         cuuint32_t estr[5] = {1, 1, (cuuint32_t)c.stride_w, (cuuint32_t)c.stride_h, 1};
         CUresult r = g_encode(&mxs, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, xhi, dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -805,52 +528,13 @@ int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_
     a.epi = c.epi;
     dim3 grid((unsigned)(n_img * a.tiles_h * a.tiles_w), (unsigned)co_tiles);
     static long long *trace = nullptr;
-    const char *trace_path = getenv("LSB_CONV_TRACE");
+    const char *trace_path = knobs().conv_trace[0] ? knobs().conv_trace : nullptr;
     if (trace_path) {
         if (!trace) cudaMalloc(&trace, (3 * 64 + 3 * 4096) * sizeof(long long));
         cudaMemsetAsync(trace, 0, (3 * 64 + 3 * 4096) * sizeof(long long), s);
         a.trace = trace;
     }
-    if (tw_t) {
-        a.tile_w = tw_t; a.tile_h = th_t; a.npix = tw_t * th_t; a.stages = st_t; a.stage_bytes = sb_t;
-        if (const char *e = getenv("LSB_CT_DBG")) a.dbg = atoi(e);
-        // output by TMA tensor store: NCHW with unit w stride and 16-B strides
-        CUtensorMap mo;
-        memset(&mo, 0, sizeof(mo));
-        if (c.so3 == 1 && c.so2 % 4 == 0 && c.so1 % 4 == 0 && c.so0 % 4 == 0 &&
-            reinterpret_cast<uintptr_t>(c.o) % 16 == 0 && tw_t % 4 == 0 && !getenv("LSB_CT_NO_TMA_OUT")) {
-            cuuint64_t dims[4] = {(cuuint64_t)c.WO, (cuuint64_t)c.HO, (cuuint64_t)CO, (cuuint64_t)n_img};
-            cuuint64_t strides[3] = {(cuuint64_t)c.so2 * 4, (cuuint64_t)c.so1 * 4, (cuuint64_t)c.so0 * 4};
-            cuuint32_t box[4] = {(cuuint32_t)tw_t, (cuuint32_t)th_t, (cuuint32_t)tc::CN_BN, 1};
-            cuuint32_t estr[4] = {1, 1, 1, 1};
-            if (g_encode(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, c.o, dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
-                a.tma_out = 1;
-        }
-        a.tiles_h = (c.HO + th_t - 1) / th_t;
-        a.tiles_w = (c.WO + tw_t - 1) / tw_t;
-        const size_t smem = (size_t)st_t * sb_t + 256 + 1024;
-        static size_t attr_t = 0;
-        if (smem > attr_t) {
-            cudaFuncSetAttribute(tc::tf32x3_conv_nhwc_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr_t = smem;
-        }
-        prof_mark(0, s);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(n_img * a.tiles_h * a.tiles_w), (unsigned)co_tiles);
-        cfg.blockDim = dim3(tc::CN_THREADS);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        cudaLaunchKernelEx(&cfg, tc::tf32x3_conv_nhwc_t_kernel, mxs, mo, a);
-        prof_mark(1, s);
-    }
-    if (!tw_t) {
+    {
         prof_mark(0, s);
         // programmatic dependent launch: the CTAs' setup (barriers, TMEM,
         // descriptor prefetch) overlaps the filter prepass's tail
@@ -907,7 +591,7 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
     constexpr int kKAlign = 32;
     const int64_t Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
     const int cfg = pick_cfg(N, K, epi.n > 0);
-    const int ilv = (cfg != 1 && !getenv("LSB_NO_ILV")) ? 1 : 0;
+    const int ilv = (cfg != 1 && !knobs().no_ilv) ? 1 : 0;
     const size_t need = sizeof(float) * (size_t)(2 * M + 2 * N) * (size_t)Kp;
     float *ws;
     int *flags;
@@ -994,6 +678,198 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
     }
     set_fast_epilogue(a, epi);
     return run_main_cfg(cfg, ahi, alo, bhi, blo, M, N, Kp, a, s, err, errlen);
+}
+
+}  // namespace lsb
+
+namespace lsb {
+
+// ---------------------------------------------------------------- planar conv
+// (conv_planar.cuh): stride 1, zero fill, any padding / dilation / strides of
+// X, W and O; one filter-image prepass + one persistent stream-K launch.
+namespace {
+std::mutex g_cp_mu;
+float *g_cp_img = nullptr, *g_cp_part = nullptr;
+size_t g_cp_img_n = 0, g_cp_part_n = 0;
+int *g_cp_flags = nullptr, *g_cp_tileflag = nullptr;   // per-tile arrival counters | [wflag, tileflag...]
+int64_t g_cp_flags_n = 0, g_cp_tileflag_n = 0;
+int *g_cp_bar = nullptr;      // grid barrier of the in-kernel filter-image build
+int64_t g_cp_bar_count = 0;   // its value after the last enqueued launch
+
+template <class T>
+bool cp_grow(T **buf, size_t *have, size_t need, bool zero, cudaStream_t s) {
+    if (need <= *have) return true;
+    if (*buf) {
+        cudaDeviceSynchronize();
+        cudaFree(*buf);
+    }
+    *buf = nullptr;
+    *have = 0;
+    if (cudaMalloc(buf, sizeof(T) * need) != cudaSuccess) return false;
+    if (zero) cudaMemsetAsync(*buf, 0, sizeof(T) * need, s);
+    *have = need;
+    return true;
+}
+
+struct CpGeom {
+    int Hp, Wp, nt, halo, tiles, co_tiles, cbs, stages;
+    int64_t units;
+};
+
+bool cp_geom(const ConvArgs &c, int64_t n_img, CpGeom &g) {
+    if (c.fill != 0.0f || c.stride_h != 1 || c.stride_w != 1 || c.dil_h < 1 || c.dil_w < 1) return false;
+    const int64_t Hp = c.HO + (c.R - 1) * c.dil_h, Wp = c.WO + (c.S - 1) * c.dil_w;
+    const int64_t nflat = n_img * Hp * Wp;
+    if (Hp < 1 || Wp < 1 || nflat >= (1ll << 30) || c.C > (1 << 20) || c.M > (1 << 20)) return false;
+    const int64_t reach = (c.R - 1) * c.dil_h * Wp + (c.S - 1) * c.dil_w;
+    // pixel tile NT (the MMA's N, a multiple of 64): the smallest of 128 / 192
+    // / 256 whose tile count fits one CTA per SM (whole tiles per CTA, no
+    // stream-K partials: C3 -> 192, 141 tiles), else 256; and the halo must fit
+    const int64_t sms = device_sms(), co_tiles = (c.M + 63) / 64;
+    g.nt = 0;
+    for (int nt : {128, 192, 256}) {
+        if (nt + reach > tc::CP_HALO) break;
+        g.nt = nt;
+        if (co_tiles * ((nflat + nt - 1) / nt) <= sms) break;
+    }
+    if (!g.nt) return false;
+    g.Hp = (int)Hp;
+    g.Wp = (int)Wp;
+    g.halo = (int)(g.nt + reach);
+    g.tiles = (int)((nflat + g.nt - 1) / g.nt);
+    g.co_tiles = (int)((c.M + 63) / 64);
+    g.cbs = (int)((c.C + 15) / 16);
+    g.stages = g.cbs * (int)(c.R * c.S);
+    g.units = (int64_t)g.co_tiles * g.tiles * g.stages;
+    return load_encode() || true;
+}
+}  // namespace
+
+bool conv_planar_ok(const ConvArgs &c, int64_t n_img) {
+    CpGeom g;
+    return cp_geom(c, n_img, g);
+}
+
+int conv_planar(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen) {
+    CpGeom g;
+    if (!cp_geom(c, n_img, g)) {
+        snprintf(err, errlen, "planar conv needs stride 1, a 0 fill and a halo <= %d rows", tc::CP_HALO);
+        return LSB_ERR_UNSUPPORTED;
+    }
+    // whole tiles per CTA when they fit one wave, else stream-K over every SM
+    const int64_t whole = (int64_t)g.co_tiles * g.tiles;
+    int ctas = (int)(whole <= device_sms() ? whole : device_sms());
+    if (knobs().cp_ctas > 0) ctas = knobs().cp_ctas;   // experiments (LSB_CP_CTAS)
+    ctas = std::max(1, std::min<int>(ctas, (int)g.units));
+    tc::ConvPlanarArgs a;
+    memset(&a, 0, sizeof(a));
+    {
+        std::lock_guard<std::mutex> lk(g_cp_mu);
+        const size_t img_n = (size_t)g.co_tiles * g.stages * (tc::CP_FSTAGE / 4);
+        const size_t part_n = (size_t)2 * ctas * 64 * g.nt;   // two segment slots per CTA
+        size_t fl = (size_t)g_cp_flags_n, tf = (size_t)g_cp_tileflag_n;
+        const bool ok = cp_grow(&g_cp_img, &g_cp_img_n, img_n, false, s) &&
+                        cp_grow(&g_cp_part, &g_cp_part_n, part_n, false, s) &&
+                        cp_grow(&g_cp_flags, &fl, (size_t)g.co_tiles * g.tiles, true, s) &&
+                        cp_grow(&g_cp_tileflag, &tf, (size_t)g.co_tiles * g.tiles + 1, true, s);
+        g_cp_flags_n = (int64_t)fl;
+        g_cp_tileflag_n = (int64_t)tf;
+        if (!ok) {
+            snprintf(err, errlen, "cudaMalloc of the planar conv workspace failed");
+            return LSB_ERR_NOMEM;
+        }
+        a.gen = ++g_gen;
+        if (a.gen <= 0) a.gen = g_gen = 1;
+        if (!g_cp_bar && cudaMalloc(&g_cp_bar, sizeof(int)) == cudaSuccess) {
+            cudaMemsetAsync(g_cp_bar, 0, sizeof(int), s);
+            g_cp_bar_count = 0;
+        }
+        if (!g_cp_bar) {
+            snprintf(err, errlen, "cudaMalloc of the planar conv barrier failed");
+            return LSB_ERR_NOMEM;
+        }
+        if (g_cp_bar_count > (1 << 30)) {   // re-zero long before the counter wraps
+            cudaMemsetAsync(g_cp_bar, 0, sizeof(int), s);
+            g_cp_bar_count = 0;
+        }
+        g_cp_bar_count += ctas;
+        a.gridbar = g_cp_bar;
+        a.bar_target = (int)g_cp_bar_count;
+    }
+    a.x = c.x;
+    a.sx[0] = c.sx0; a.sx[1] = c.sx1; a.sx[2] = c.sx2; a.sx[3] = c.sx3;
+    a.N = (int)n_img; a.C = (int)c.C; a.H = (int)c.H; a.W = (int)c.W; a.CO = (int)c.M;
+    a.R = (int)c.R; a.S = (int)c.S; a.HO = (int)c.HO; a.WO = (int)c.WO;
+    a.ph = (int)c.pad_h; a.pw = (int)c.pad_w; a.dh = (int)c.dil_h; a.dw = (int)c.dil_w;
+    a.Hp = g.Hp; a.Wp = g.Wp; a.halo = g.halo;
+    a.tiles = g.tiles; a.co_tiles = g.co_tiles; a.cbs = g.cbs; a.stages = g.stages; a.units = g.units;
+    a.wimg = g_cp_img;
+    a.wimg_w = g_cp_img;
+    a.o = c.o;
+    a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
+    a.part = g_cp_part;
+    a.tilecnt = g_cp_flags;
+    a.wflag = g_cp_tileflag;
+    a.tileflag = g_cp_tileflag + 1;
+    a.w = c.w;
+    a.swt[0] = c.sw0; a.swt[1] = c.sw1; a.swt[2] = c.sw2; a.swt[3] = c.sw3;
+    a.epi = c.epi;
+    a.dbg = knobs().cp_dbg;
+    if (aux_launches) *aux_launches = 0;
+    static bool attr[3] = {false, false, false};
+    const int which = g.nt == 256 ? 2 : g.nt == 192 ? 1 : 0;
+    const void *kfn = which == 2 ? (const void *)tc::conv_planar_kernel<256>
+                      : which == 1 ? (const void *)tc::conv_planar_kernel<192>
+                                   : (const void *)tc::conv_planar_kernel<128>;
+    if (!attr[which]) {
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::CP_SMEM);
+        attr[which] = true;
+    }
+    static long long *trace = nullptr;
+    const char *trace_path = knobs().conv_trace[0] ? knobs().conv_trace : nullptr;
+    if (trace_path) {
+        if (!trace) cudaMalloc(&trace, 148 * 192 * sizeof(long long));
+        cudaMemsetAsync(trace, 0, 148 * 192 * sizeof(long long), s);
+        a.trace = trace;
+    }
+    prof_mark(0, s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3(tc::CP_THREADS);
+    cfg.dynamicSmemBytes = tc::CP_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;   // the filter-image grid barrier: all CTAs resident
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (knobs().cp_dbg & 512) ? 0 : 1;   // experiments: plain launch
+    void *args[] = {&a};
+    cudaError_t e = cudaLaunchKernelExC(&cfg, kfn, args);
+    prof_mark(1, s);
+    if (e != cudaSuccess) {
+        snprintf(err, errlen, "conv_planar launch (%d CTAs): %s", ctas, cudaGetErrorString(e));
+        return LSB_ERR_CUDA;
+    }
+    if (trace_path) {
+        static long long h[148 * 192];
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
+        if (FILE *f = fopen(trace_path, "w")) {
+            fprintf(f, "# ctas %d units %lld tiles %d stages %d nt %d\n", ctas, (long long)g.units, g.tiles,
+                    g.stages, g.nt);
+            for (int b = 0; b < ctas; b++) {
+                for (int k = 0; k < 64; k++) fprintf(f, "%lld ", h[b * 64 + k]);
+                fprintf(f, "\n");
+            }
+            for (int b = 0; b < ctas; b++) {
+                fprintf(f, "S ");
+                for (int k = 0; k < 128; k++) fprintf(f, "%lld ", h[148 * 64 + b * 128 + k]);
+                fprintf(f, "\n");
+            }
+            fclose(f);
+        }
+    }
+    return LSB_OK;
 }
 
 }  // namespace lsb

@@ -65,6 +65,66 @@ int check_device() {
 int lsb::device_sms() { return sm_count(); }
 
 namespace {
+lsb::Knobs g_knobs;
+std::once_flag g_knobs_once;
+std::mutex g_knobs_mu;
+
+void read_knobs(lsb::Knobs &k) {
+    memset(&k, 0, sizeof(k));
+    auto on = [](const char *n) { return getenv(n) != nullptr; };
+    auto num = [](const char *n) { const char *e = getenv(n); return e ? atoi(e) : 0; };
+    auto str = [](const char *n, char *dst) {
+        const char *e = getenv(n);
+        snprintf(dst, 256, "%s", e ? e : "");
+    };
+    k.gemm_algo = LSB_ALGO_AUTO;
+    if (const char *e = getenv("LSB_GEMM_ALGO")) {
+        if (!strcmp(e, "simt")) k.gemm_algo = LSB_ALGO_SIMT;
+        else if (!strcmp(e, "tf32x3")) k.gemm_algo = LSB_ALGO_TF32X3;
+        else if (!strcmp(e, "tf32x3_nhwc")) k.gemm_algo = lsb::kAlgoTf32x3Nhwc;
+        else if (!strcmp(e, "tf32x3_planar")) k.gemm_algo = lsb::kAlgoTf32x3Planar;
+    }
+    k.tc_cfg = -1;
+    if (const char *e = getenv("LSB_TC_CFG")) {
+        if (!strcmp(e, "16x128")) k.tc_cfg = 0;
+        else if (!strcmp(e, "32x128")) k.tc_cfg = 1;
+        else if (!strcmp(e, "16x256")) k.tc_cfg = 2;
+    }
+    if (const char *e = getenv("LSB_MP_MODE")) k.mp_mode = !strcmp(e, "cluster") ? 1 : !strcmp(e, "streamk") ? 2 : 0;
+    k.fixup_ctas = num("LSB_FIXUP_CTAS");
+    k.mp_cluster = num("LSB_MP_CLUSTER");
+    k.streamk_ctas = num("LSB_STREAMK_CTAS");
+    k.conv_splits = num("LSB_CONV_SPLITS");
+    k.cp_dbg = num("LSB_CP_DBG");
+    k.cp_ctas = num("LSB_CP_CTAS");
+    k.scalar_split = on("LSB_SCALAR_SPLIT");
+    k.no_pair = on("LSB_NO_PAIR");
+    k.no_tail_split = on("LSB_NO_TAIL_SPLIT");
+    k.no_persist = on("LSB_NO_PERSIST");
+    k.no_fast_epi = on("LSB_NO_FAST_EPI");
+    k.no_ilv = on("LSB_NO_ILV");
+    k.no_small = on("LSB_NO_SMALL");
+    k.no_streamk = on("LSB_NO_STREAMK");
+    k.no_mp_fast = on("LSB_NO_MP_FAST");
+    k.no_mp_cluster = on("LSB_NO_MP_CLUSTER");
+    k.no_conv_split = on("LSB_NO_CONV_SPLIT");
+    str("LSB_GEMM_TRACE", k.gemm_trace);
+    str("LSB_CONV_TRACE", k.conv_trace);
+}
+}  // namespace
+
+const lsb::Knobs &lsb::knobs() {
+    std::call_once(g_knobs_once, [] { read_knobs(g_knobs); });
+    return g_knobs;
+}
+
+void lsb::reload_knobs() {
+    knobs();
+    std::lock_guard<std::mutex> lk(g_knobs_mu);
+    read_knobs(g_knobs);
+}
+
+namespace {
 bool g_prof = false;
 cudaEvent_t g_prof_ev[2] = {nullptr, nullptr};
 }  // namespace
@@ -197,10 +257,8 @@ int pick_mode_b(const lsb_gemm_desc *d) {
 // computed); -1 when an explicit request cannot be honoured
 int select_algo(const lsb_gemm_desc *d, int64_t M) {
     int algo = d->algo;
-    if (const char *env = getenv("LSB_GEMM_ALGO")) {
-        if (!strcmp(env, "simt")) algo = LSB_ALGO_SIMT;
-        else if (!strcmp(env, "tf32x3")) algo = LSB_ALGO_TF32X3;
-    }
+    const int forced = lsb::knobs().gemm_algo;
+    if (forced == LSB_ALGO_SIMT || forced == LSB_ALGO_TF32X3) algo = forced;
     const bool tc_ok = d->combine == LSB_OP_MUL && d->reduce == LSB_OP_ADD && !d->beta_in_loop &&
                        d->batch == 1 && d->K > 0;
     if (algo == LSB_ALGO_TF32X3) return tc_ok ? algo : -1;
@@ -222,6 +280,11 @@ int lsb_gemm_algo(const lsb_gemm_desc *d) {
 }
 
 int lsb_abi_version(void) { return LSB_ABI_VERSION; }
+
+int lsb_reload_env(void) {
+    lsb::reload_knobs();
+    return LSB_OK;
+}
 
 int lsb_last_error(char *buf, size_t len) {
     if (buf && len) {
@@ -448,7 +511,7 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
         d->K <= 1024 && d->K % 4 == 0 && d->N % 4 == 0 && (double)M * d->N * d->K * d->batch <= (double)(1 << 26) &&
         d->sa_k == 1 && d->sa_m % 4 == 0 && aligned16(a.A) && d->sb_n == 1 && d->sb_k % 4 == 0 &&
         aligned16(d->B) && (d->batch == 1 || (d->sa_b % 4 == 0 && d->sb_b % 4 == 0)) && d->batch <= 65535 &&
-        !getenv("LSB_NO_SMALL")) {
+        !lsb::knobs().no_small) {
         lsb::prof_mark(0, s);
         const int lrc = lsb::launch_small_gemm(d->combine, d->reduce, a, d->batch, s);
         lsb::prof_mark(1, s);
@@ -484,22 +547,22 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
         const int64_t t128 = ((M + 127) / 128) * n_tiles;
         if (d->combine == LSB_OP_ADD && (d->reduce == LSB_OP_MAX || d->reduce == LSB_OP_MIN) &&
             !d->beta_in_loop && d->beta == 1.0f && a.epi.n == 0 && d->batch == 1 && d->split_k == 0 &&
-            t128 < 3 * slots && d->K >= 64 * lsb::kBK && !getenv("LSB_NO_STREAMK")) {
+            t128 < 3 * slots && d->K >= 64 * lsb::kBK && !lsb::knobs().no_streamk) {
             // row-major 16-B aligned operands with K % 16 == 0 (C2): the
             // cp.async kernel with 16-deep slices (maxplus_fast.cuh)
             const bool fast = d->sa_k == 1 && d->sa_m % 4 == 0 && aligned16(a.A) && d->sb_n == 1 &&
                               d->sb_k % 4 == 0 && aligned16(d->B) && d->N % 4 == 0 && d->K % 16 == 0 &&
-                              !getenv("LSB_NO_MP_FAST");
+                              !lsb::knobs().no_mp_fast;
             // split-K over a cluster with a DSMEM reduction: one launch, no
             // fill, no atomics; cluster size S from the slot-wave cost model
             // (C2: 64 tiles x 4 = 256 CTAs: 78.6 us vs 87 us stream-K)
             // default: stream-K with the in-kernel fixup (every SM the same
             // slice count); LSB_MP_MODE=cluster|streamk selects the others
-            const char *mode = getenv("LSB_MP_MODE");
-            if (fast && (!mode || !strcmp(mode, "fixup"))) {
+            const int mode = lsb::knobs().mp_mode;
+            if (fast && mode == 0) {
                 const int64_t units = t128 * (d->K / 16);
                 int ctas = lsb::maxplus_fixup_ctas(units);
-                if (const char *e = getenv("LSB_FIXUP_CTAS")) ctas = std::max(1, std::min(ctas, atoi(e)));
+                if (lsb::knobs().fixup_ctas > 0) ctas = std::max(1, std::min(ctas, lsb::knobs().fixup_ctas));
                 if (ctas >= 1) {
                     float4 *part = nullptr;
                     int *flags = nullptr, epoch = 0;
@@ -513,7 +576,7 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
                     return check_launch("maxplus_fixup");
                 }
             }
-            if (fast && !getenv("LSB_NO_MP_CLUSTER") && !(mode && !strcmp(mode, "streamk"))) {
+            if (fast && !lsb::knobs().no_mp_cluster && mode != 2) {
                 int best_s = 0;
                 double best = 1e30;
                 // powers of two only: 3-, 5-, 6-, 7- and 9-CTA clusters measured
@@ -523,7 +586,7 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
                     const double cost = (double)((t128 * sp + slots - 1) / slots) / sp + 0.002 * sp;
                     if (cost < best - 1e-12) { best = cost; best_s = sp; }
                 }
-                if (const char *e = getenv("LSB_MP_CLUSTER")) best_s = atoi(e);
+                if (lsb::knobs().mp_cluster > 0) best_s = lsb::knobs().mp_cluster;
                 if (best_s >= 2) {
                     lsb::prof_mark(0, s);
                     const int lrc = lsb::launch_maxplus_cluster(d->reduce, a, best_s, s);
@@ -535,7 +598,7 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
             }
             const int64_t units = t128 * (fast ? d->K / 16 : (d->K + lsb::kBK - 1) / lsb::kBK);
             int ctas = (int)std::min<int64_t>(slots, std::max<int64_t>(1, units / (fast ? 8 : 16)));
-            if (const char *e = getenv("LSB_STREAMK_CTAS")) ctas = std::max(1, atoi(e));
+            if (lsb::knobs().streamk_ctas > 0) ctas = lsb::knobs().streamk_ctas;
             lsb::prof_mark(0, s);
             if (fast) lsb::launch_streamk_fast(d->reduce, a, ctas, s);
             else lsb::launch_streamk(d->reduce, a, ctas, s);
@@ -623,35 +686,32 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     const bool wcontig = d->sw[3] == 1 && d->sw[2] == d->S && d->sw[1] == d->R * d->S;
     a.a_mode = (wcontig && aligned16(d->w) && d->sw[0] % 4 == 0 && K % 4 == 0) ? lsb::LD_VEC_K : lsb::LD_GENERIC;
 
-    // tensor cores: in-kernel im2col + 3xTF32 (tf32x3_conv.cuh) for real work
-    // and C*R*S <= 1024; the materialised-im2col variant (8*P*K bytes of
-    // prepass, slower than SIMT on C3: 0.185 vs 0.101 ms) only on request
-    // tc_mode: 4 = NHWC hi/lo copy + pure TMA->MMA, 3 = TMA-fed raw NCHW
-    // boxes + converter warps, 1 = in-kernel gather, 2 = materialised im2col
-    // (on request only), 0 = SIMT
+    // tensor cores (split TF32) for real work: the NHWC-copy kernel
+    // (tf32x3_conv_nhwc.cuh: zero fill, strides <= 8) or the planar
+    // single-launch kernel (conv_planar.cuh: stride 1, zero fill); SIMT
+    // otherwise (nonzero fill, tiny convs).
+    // LSB_GEMM_ALGO=simt|tf32x3|tf32x3_nhwc|tf32x3_planar.
+    // Measured on C3 (tools/bench_c3.py, L2 flushed): NHWC-copy
+    // 26.7 us per step, planar 27.6 us -- the NHWC kernel first, the planar
+    // one for stride-1 convs the NHWC kernel cannot take (N*H > 65535).
     const bool big = 2.0 * a.M * a.N * d->N * K >= (double)(1ll << 28) && a.M >= 16;
-    const bool nhwc_ok = lsb::tf32x3_conv_nhwc_ok(a, d->N);
-    const bool tma_ok = lsb::tf32x3_conv_tma_ok(a, d->N), gather_ok = lsb::tf32x3_conv_direct_ok(a, d->N);
-    // auto-selection uses only the NHWC kernel: it alone recomputes tiles
-    // with non-finite inputs exactly; the others are on request
-    int tc_mode = big && nhwc_ok ? 4 : 0;
-    if (const char *env = getenv("LSB_GEMM_ALGO")) {
-        if (!strcmp(env, "simt")) tc_mode = 0;
-        else if (!strcmp(env, "tf32x3")) tc_mode = nhwc_ok ? 4 : tma_ok ? 3 : gather_ok ? 1 : 2;
-        else if (!strcmp(env, "tf32x3_tma")) tc_mode = tma_ok ? 3 : 2;
-        else if (!strcmp(env, "tf32x3_gather")) tc_mode = gather_ok ? 1 : 2;
-        else if (!strcmp(env, "tf32x3_im2col")) tc_mode = 2;
+    const bool planar_ok = lsb::conv_planar_ok(a, d->N), nhwc_ok = lsb::tf32x3_conv_nhwc_ok(a, d->N);
+    int tc_mode = !big ? 0 : nhwc_ok ? 4 : planar_ok ? 5 : 0;
+    switch (lsb::knobs().gemm_algo) {
+    case LSB_ALGO_SIMT: tc_mode = 0; break;
+    case LSB_ALGO_TF32X3: tc_mode = nhwc_ok ? 4 : planar_ok ? 5 : 0; break;
+    case lsb::kAlgoTf32x3Nhwc: tc_mode = nhwc_ok ? 4 : planar_ok ? 5 : 0; break;
+    case lsb::kAlgoTf32x3Planar: tc_mode = planar_ok ? 5 : nhwc_ok ? 4 : 0; break;
+    default: break;
     }
     if (tc_mode) {
         char err[256] = "";
         int aux = 0;
         cudaStream_t st = (cudaStream_t)stream;
-        rc = tc_mode == 4   ? lsb::tf32x3_conv_nhwc(a, d->N, st, &aux, err, sizeof(err))
-             : tc_mode == 3 ? lsb::tf32x3_conv_tma(a, d->N, st, &aux, err, sizeof(err))
-             : tc_mode == 1 ? lsb::tf32x3_conv_direct(a, d->N, st, &aux, err, sizeof(err))
-                            : lsb::tf32x3_conv(a, d->N, st, &aux, err, sizeof(err));
+        rc = tc_mode == 5 ? lsb::conv_planar(a, d->N, st, &aux, err, sizeof(err))
+                          : lsb::tf32x3_conv_nhwc(a, d->N, st, &aux, err, sizeof(err));
         if (rc) return fail(rc, "%s", err);
-        rc = check_launch("tf32x3_conv");
+        rc = check_launch(tc_mode == 5 ? "conv_planar" : "tf32x3_conv_nhwc");
         if (rc) return rc;
         g_launches.fetch_add(aux, std::memory_order_relaxed);
         return LSB_OK;
@@ -665,7 +725,7 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     {
         const int64_t slots = (int64_t)sm_count() * 2;
         const int64_t k_slices = (K + lsb::kBK - 1) / lsb::kBK;
-        if (tiles < 2 * slots && k_slices >= 16 && !getenv("LSB_NO_CONV_SPLIT")) {
+        if (tiles < 2 * slots && k_slices >= 16 && !lsb::knobs().no_conv_split) {
             // cost = the busiest SM's CTA count x work per CTA (+ fold traffic)
             const int64_t sms = sm_count();
             double best = 1e30;
@@ -675,7 +735,7 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
                 if (cost < best - 1e-9) { best = cost; splits = s; }
             }
         }
-        if (const char *e = getenv("LSB_CONV_SPLITS")) splits = std::max(1, atoi(e));
+        if (lsb::knobs().conv_splits > 0) splits = lsb::knobs().conv_splits;
     }
     int64_t kps = (K + splits - 1) / splits;
     kps = (kps + lsb::kBK - 1) / lsb::kBK * lsb::kBK;

@@ -13,6 +13,24 @@ using SplitFn = void (*)(const GemmArgs &, int64_t, cudaStream_t);
 using NestFn = void (*)(const NestArgs &, cudaStream_t);
 
 int device_sms();                               // lsb_api.cu
+
+// Environment knobs, read once -- at the first use or on
+// lsb_reload_env() -- never on the launch path.  Defaults are the measured best.
+constexpr int kAlgoTf32x3Nhwc = 3;     // LSB_GEMM_ALGO=tf32x3_nhwc (convs: the NHWC-copy kernel)
+constexpr int kAlgoTf32x3Planar = 4;   // LSB_GEMM_ALGO=tf32x3_planar (convs: the planar kernel)
+struct Knobs {
+    int gemm_algo;        // LSB_GEMM_ALGO: LSB_ALGO_AUTO | LSB_ALGO_SIMT | LSB_ALGO_TF32X3 | kAlgoTf32x3Nhwc
+    int tc_cfg;           // LSB_TC_CFG: -1 auto, 0 = 16x128, 1 = 32x128, 2 = 16x256
+    int mp_mode;          // LSB_MP_MODE: 0 fixup, 1 cluster, 2 streamk
+    int fixup_ctas, mp_cluster, streamk_ctas, conv_splits;   // 0 = model's choice
+    int cp_dbg;           // LSB_CP_DBG: planar conv timing experiments (conv_planar.cuh)
+    int cp_ctas;          // LSB_CP_CTAS: planar conv grid size (0 = one CTA per SM)
+    bool scalar_split, no_pair, no_tail_split, no_persist, no_fast_epi, no_ilv;
+    bool no_small, no_streamk, no_mp_fast, no_mp_cluster, no_conv_split;
+    char gemm_trace[256], conv_trace[256];   // "" = off
+};
+const Knobs &knobs();
+void reload_knobs();
 // optional timing of the dominant kernel of a call (lsb_profile): which = 0
 // before its launch, 1 after; no-op unless profiling is enabled
 void prof_mark(int which, cudaStream_t s);
@@ -36,17 +54,13 @@ bool tf32x3_supported(int64_t M, int64_t N, int64_t K);
 int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, int64_t sa_k, const float *B,
                 int64_t sb_k, int64_t sb_n, float *C, int64_t sc_m, int64_t sc_n, int c_vec, const EpiStages &epi,
                 bool b_unchanged, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
-int tf32x3_conv(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
-bool tf32x3_conv_direct_ok(const ConvArgs &c, int64_t n_img);
-bool tf32x3_conv_tma_ok(const ConvArgs &c, int64_t n_img);
 int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec, cudaStream_t s, int *aux_launches,
                         char *err, size_t errlen);
 bool tf32x3_conv_nhwc_ok(const ConvArgs &c, int64_t n_img);
 int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err,
                      size_t errlen);
-int tf32x3_conv_tma(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
-int tf32x3_conv_direct(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err,
-                       size_t errlen);
+bool conv_planar_ok(const ConvArgs &c, int64_t n_img);
+int conv_planar(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
 
 template <int C, int R, bool B, int BM, bool TWO = false>
 void launch_gemm(const GemmArgs &a, dim3 grid, cudaStream_t s) {

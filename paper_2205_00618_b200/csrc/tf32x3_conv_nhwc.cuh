@@ -21,7 +21,7 @@
 // Tile: 4 output rows x 32 output columns of one image (M = 128), 64 channels.
 #pragma once
 
-#include "tf32x3_conv_tma.cuh"
+#include "conv_common.cuh"
 
 namespace lsb {
 namespace tc {
@@ -56,24 +56,7 @@ struct ConvNhwcArgs {
     int64_t C, H, W, sx[4], swt[4];
     EpiStages epi;
     long long *trace;     // debug (LSB_CN_TRACE builds): per-stage clock64 stamps of CTA 0
-    // channel-major variant (tf32x3_conv_nhwc_t_kernel): output tile of
-    // tile_h x tile_w pixels (npix = N of the MMA), `stages` ring slots of
-    // stage_bytes each
-    int tile_h, tile_w, npix, stages, stage_bytes;
-    int dbg;              // experiments (LSB_CT_DBG): 1 = skip the output stores
-    int tma_out;          // output tile leaves by one TMA tensor store (map_o)
 };
-
-// TMA tensor store of a dense smem box [co][h][w] to NCHW (out-of-range
-// coordinates are clipped by the hardware)
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, const void *src, int c0, int c1, int c2, int c3) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-            reinterpret_cast<uint64_t>(map)),
-        "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-        : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
 
 #ifdef LSB_CN_TRACE
 #define CN_TRACE(ev, kb)                                                                          \
@@ -422,275 +405,6 @@ __global__ void __launch_bounds__(CN_THREADS, 2)
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CN_CHUNKS * CN_ACC_COLS));
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Channel-major variant: D[co][pixel] instead of D[pixel][co].
-//
-// The MMA's A operand is the filter stage image itself -- 128 rows = Whi for
-// 64 output channels, then Wlo for the same channels (K-major SW64, the
-// 8 KiB bulk copy above) -- and B is an X box of npix = tile_h x tile_w
-// pixels (K-major SW128 rows [hi16 | lo16], B_lo = B_hi + 64 B).  Per 8
-// channels two MMAs of 128 x npix x 8:
-//     D += [Whi; Wlo] . Xhi      D += [Whi; Wlo] . Xlo
-// so for channel co = 16q + c TMEM row 32q + 2c collects Whi.(Xhi + Xlo) and
-// row 32q + 2c + 1 Wlo.(Xhi + Xlo) (the filter image interleaves the hi and
-// lo rows of a channel, FilterImgArgs::ilv_rows); the epilogue adds them
-// with one warp shuffle (4 split terms, lo.lo included).
-// Why: a 128 x N x 8 tf32 MMA costs ~87 cycles for any N <= 128 and ~135 at
-// N = 256 (tools/umma_mn_test.cu), so the pixel-major kernel's N = 64 + N = 128
-// pair spends 348 cycles per 16 channels on 128 pixels, this one ~2 x 2 x 125
-// on 224 (C3: a 4 x 56 pixel tile, 112 tiles, one CTA per SM).
-// Epilogue: TMEM -> shuffle sum -> dense smem box S[64][npix] -> one TMA
-// tensor store into NCHW (or row stores when the strides do not allow it).
-constexpr int CT_MAX_STAGES = 8;
-
-__global__ void __launch_bounds__(CN_THREADS, 1)
-    tf32x3_conv_nhwc_t_kernel(const __grid_constant__ CUtensorMap map_xs, const __grid_constant__ CUtensorMap map_o,
-                              const ConvNhwcArgs p) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int NST = p.stages, SB = p.stage_bytes, NP = p.npix;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * SB);
-    uint64_t *empty = full + CT_MAX_STAGES;
-    uint64_t *tdone = empty + CT_MAX_STAGES;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tdone + 1);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int64_t t = blockIdx.x;
-    const int tw = (int)(t % p.tiles_w);
-    t /= p.tiles_w;
-    const int th = (int)(t % p.tiles_h);
-    const int n = (int)(t / p.tiles_h);
-    const int h0 = th * p.tile_h, w0 = tw * p.tile_w;
-    const int64_t c0 = (int64_t)blockIdx.y * CN_BN;
-    const int cblocks = (int)(p.Cp / CN_BK);
-    const int num_kb = (int)(p.R * p.S) * cblocks;
-    const int xbytes = NP * 128;
-    if (threadIdx.x == 0) CN_TRACE(2, 2);
-
-    if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&map_xs);
-        for (int s = 0; s < NST; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        mbar_init(tdone, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        // ---------------- TMA producer: X box (npix rows) + filter stage image
-        if (lane == 0) {
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            const int hin0 = (int)(h0 * p.sh - p.ph), win0 = (int)(w0 * p.sw - p.pw);
-            int stage = 0;
-            uint32_t phase = 0;
-            int cb = 0, s = 0, r = 0;
-            for (int kb = 0; kb < num_kb; kb++) {
-                mbar_wait(&empty[stage | 1], phase ^ 1);   // slot pairs released together
-                CN_TRACE(0, kb);
-                unsigned char *base = smem + stage * SB;
-                mbar_expect_tx(&full[stage], xbytes + CN_TILE_B);
-                const int hi_ = hin0 + r * (int)p.dh, wi = win0 + s * (int)p.dw;
-                tma_load_5d(&map_xs, &full[stage], base, 0, cb, wi, hi_, n);
-                bulk_load(base + xbytes, p.wimg + ((int64_t)blockIdx.y * num_kb + kb) * (2 * CN_BN * CN_BK),
-                          CN_TILE_B, &full[stage]);
-                if (++cb == cblocks) {
-                    cb = 0;
-                    if (++s == p.S) {
-                        s = 0;
-                        ++r;
-                    }
-                }
-                if (++stage == NST) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer: A = filter image (SW64), B = X box (SW128)
-        if (lane == 0) {
-            const uint32_t idesc = idesc_tf32(128, NP);
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int kb = 0; kb < num_kb; kb++) {
-                mbar_wait(&full[stage], phase);
-                CN_TRACE(1, kb);
-                tc_fence_after();
-                const int chunk = kb / p.stages_per_chunk;
-                const uint32_t d = tmem + (uint32_t)(chunk * 256);
-                const uint32_t base = smem_u32(smem + stage * SB);
-                const uint64_t bhi = sdesc_k_sw<128>(base), blo = bhi + (uint64_t)(64 >> 4);
-                const uint64_t aw = sdesc_k_sw<64>(base + xbytes);
-#pragma unroll
-                for (int k = 0; k < CN_BK / 8; k++) {
-                    const uint64_t off = (uint64_t)((k * 32) >> 4);
-                    const uint32_t first = (kb % p.stages_per_chunk == 0 && k == 0) ? 0u : 1u;
-                    umma_tf32(d, aw + off, bhi + off, idesc, first);
-                    umma_tf32(d, aw + off, blo + off, idesc, 1u);
-                }
-                if (stage & 1) umma_commit(&empty[stage]);
-                if (++stage == NST) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-            umma_commit(tdone);
-        }
-    } else {
-        // ---------------- epilogue (warps 2..9)
-        // A rows are interleaved per channel (filter image ilv_rows): TMEM
-        // lane 32q + 2c holds Whi.X and lane 32q + 2c + 1 Wlo.X of channel
-        // 16q + c, so one shuffle sums them inside the warp that owns the
-        // lane quarter; even lanes then write S[co][pix] (dense NCHW box).
-        const int ew = warp - 2;
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        mbar_wait(tdone, 0);
-        if (ew == 0 && lane == 0) CN_TRACE(2, 0);
-        tc_fence_after();
-        // S[64][NP + 8]: a channel's tile rows dense (one TMA box per channel);
-        // the 8-float pad puts the 8 float4 stores of a quarter-warp (4
-        // channels x 2 lanes) in 8 distinct bank groups
-        const int SP = NP + 8;
-        float *S = reinterpret_cast<float *>(smem);
-        const bool nonfinite = *p.anyflag == p.gen;
-        if (!nonfinite) {
-            const int qd = warp & 3, half = ew >> 2;
-            const int co_l = 16 * qd + (lane >> 1);
-            const int nch = (num_kb + p.stages_per_chunk - 1) / p.stages_per_chunk;
-            for (int part = half; part < NP / 16; part += 2) {
-                const int col = part * 16;
-                uint32_t rr[CN_CHUNKS][16];
-#pragma unroll
-                for (int ch = 0; ch < CN_CHUNKS; ch++)
-                    if (ch < nch)
-                        tmem_ld16_issue(tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ch * 256 + col), rr[ch]);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                float v[16];
-#pragma unroll
-                for (int i = 0; i < 16; i++) {
-                    float acc = __uint_as_float(rr[0][i]);
-#pragma unroll
-                    for (int ch = 1; ch < CN_CHUNKS; ch++)
-                        if (ch < nch) acc += __uint_as_float(rr[ch][i]);
-                    v[i] = acc + __shfl_xor_sync(0xffffffffu, acc, 1);   // hi row + lo row
-                }
-                // both lanes of the pair hold the sums: lane half h stores
-                // float4s h and h + 2 of the 16 columns
-                const int h4 = (lane & 1) * 4;
-#pragma unroll
-                for (int q = 0; q < 2; q++) {
-                    float x[4];
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        // static register index: select between the two halves
-                        x[e] = (lane & 1) ? v[q * 8 + 4 + e] : v[q * 8 + e];
-                        if (p.epi.n) {
-                            const int pix = col + q * 8 + h4 + e;
-                            x[e] = apply_epilogue(p.epi, x[e], n, c0 + co_l, h0 + pix / p.tile_w, w0 + pix % p.tile_w);
-                        }
-                    }
-                    *reinterpret_cast<float4 *>(S + co_l * SP + col + q * 8 + h4) = make_float4(x[0], x[1], x[2], x[3]);
-                }
-            }
-        }
-        if (ew == 0 && lane == 0) CN_TRACE(2, 3);
-        tc_fence_before();
-        asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
-        if (ew == 0 && lane == 0) CN_TRACE(2, 4);
-        if (nonfinite) {
-            // non-finite input somewhere: FP32 recompute of the tile
-            for (int i = threadIdx.x - 64; i < CN_BN * NP; i += CN_EPI_WARPS * 32) {
-                const int co_l = i / NP, pix = i % NP;
-                const int ho = h0 + pix / p.tile_w, wo = w0 + pix % p.tile_w;
-                const int64_t co = c0 + co_l;
-                float acc = 0.0f;
-                if (co < p.CO && ho < p.HO && wo < p.WO) {
-                    for (int64_t c = 0; c < p.C; c++)
-                        for (int64_t r = 0; r < p.R; r++) {
-                            const int64_t hi_ = ho * p.sh - p.ph + r * p.dh;
-                            for (int64_t s2 = 0; s2 < p.S; s2++) {
-                                const int64_t wi = wo * p.sw - p.pw + s2 * p.dw;
-                                const bool in = hi_ >= 0 && hi_ < p.H && wi >= 0 && wi < p.W;
-                                const float xv =
-                                    in ? p.x[n * p.sx[0] + c * p.sx[1] + hi_ * p.sx[2] + wi * p.sx[3]] : 0.0f;
-                                acc = fmaf(xv, p.w[co * p.swt[0] + c * p.swt[1] + r * p.swt[2] + s2 * p.swt[3]], acc);
-                            }
-                        }
-                    if (p.epi.n) acc = apply_epilogue(p.epi, acc, n, co, ho, wo);
-                }
-                S[co_l * SP + pix] = acc;
-            }
-            asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
-        }
-        if (ew == 0 && lane == 0) CN_TRACE(2, 5);
-        if (p.tma_out) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
-            // repack into the dense box D[64][NP] (float4 along pixels: both
-            // sides conflict-free; loads batched before stores), then one
-            // TMA tensor store of the whole tile
-            float *D = S + ((CN_BN * SP + 255) & ~255);
-            const int q4 = NP / 4;
-            const int tid = threadIdx.x - 64;
-            for (int e0 = tid; e0 < CN_BN * q4; e0 += 4 * CN_EPI_WARPS * 32) {
-                float4 x[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int e = e0 + u * CN_EPI_WARPS * 32;
-                    if (e < CN_BN * q4) {
-                        const int co_l = e / q4, px = (e - co_l * q4) * 4;
-                        x[u] = *reinterpret_cast<const float4 *>(S + co_l * SP + px);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const int e = e0 + u * CN_EPI_WARPS * 32;
-                    if (e < CN_BN * q4) reinterpret_cast<float4 *>(D)[e] = x[u];
-                }
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("bar.sync 1, %0;" ::"r"(CN_EPI_WARPS * 32) : "memory");
-            if (ew == 0 && lane == 0) {
-                if (!(p.dbg & 1)) tma_store_4d(&map_o, D, w0, h0, (int)c0, n);
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            }
-        } else {
-            // (channel, output row) pairs; lanes along the row
-            for (int rw = ew; rw < ((p.dbg & 1) ? 0 : CN_BN * p.tile_h); rw += CN_EPI_WARPS) {
-                const int co_l = rw / p.tile_h, h = rw % p.tile_h;
-                const int64_t co = c0 + co_l;
-                const int ho = h0 + h;
-                if (co >= p.CO || ho >= p.HO) continue;
-                float *orow = p.o + n * p.so[0] + co * p.so[1] + (int64_t)ho * p.so[2];
-                const float *srow = S + co_l * SP + h * p.tile_w;
-                for (int w = lane; w < p.tile_w; w += 32) {
-                    const int wo = w0 + w;
-                    if (wo >= p.WO) break;
-                    orow[(int64_t)wo * p.so[3]] = srow[w];
-                }
-            }
-        }
-    }
-    if (warp == 2 && lane == 0) CN_TRACE(2, 7);
-    tc_fence_before();
-    __syncthreads();
-    if (threadIdx.x == 0) CN_TRACE(2, 1);
-    if (warp == 1) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
 }
 

@@ -73,11 +73,6 @@ struct TcArgs {
     int mt2, nt2;            // its CTAs follow the first rectangle's
     float *C; int64_t sc_m, sc_n;
     int c_vec;
-    // conv mode (conv_hw > 0): m = output channel, n = pixel = (img, ho, wo);
-    // element address img*so[0] + m*so[1] + ho*so[2] + wo*so[3], epilogue
-    // coordinates (img, co, ho, wo) like lsb_conv2d_nchw
-    int64_t conv_hw, conv_wo;
-    int64_t so[4];
     EpiStages epi;
     // fast epilogue (fast_n stages, each "+ bias[n * stride]" if bias != null,
     // then ReLU if relu): set by the host when every stage has that form
@@ -404,93 +399,6 @@ __global__ void __launch_bounds__(256) tf32_split_rcontig_kernel(const float *__
             flag[r] = gen;
             *any = gen;
         }
-    }
-}
-
-// Conv prepass: im2col + split of the input.  Row p = output pixel
-// (img, ho, wo), column k = tap (c, r, s); out-of-range taps take the view's
-// oob `fill`.  32 pixels x 32 taps per block: read with pixels fastest (wo
-// runs along the input's w stride), write k-fastest through smem.
-struct ConvGeom {
-    int64_t C, H, W, R, S, HO, WO, P, K, Kp;
-    int64_t sh, sw, ph, pw, dh, dw;
-    int64_t sx0, sx1, sx2, sx3;
-    float fill;
-    const float *x;   // input (used by the in-kernel im2col conv)
-};
-
-__global__ void __launch_bounds__(256) im2col_split_kernel(const float *__restrict__ x, const ConvGeom g,
-                                                           float *__restrict__ hi, float *__restrict__ lo) {
-    __shared__ float tile[32][33];
-    const int64_t p0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int64_t hw = g.HO * g.WO, rs = g.R * g.S;
-    const int64_t pix = p0 + tx;
-    int64_t img = 0, ho = 0, wo = 0;
-    if (pix < g.P) {
-        img = pix / hw;
-        ho = (pix % hw) / g.WO;
-        wo = pix % g.WO;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-        const int a = ty + 8 * j;
-        const int64_t k = k0 + a;
-        float v = 0.0f;
-        if (pix < g.P && k < g.K) {
-            const int64_t c = k / rs, r = (k % rs) / g.S, s = k % g.S;
-            const int64_t hi_ = ho * g.sh + r * g.dh - g.ph, wi = wo * g.sw + s * g.dw - g.pw;
-            v = (hi_ >= 0 && hi_ < g.H && wi >= 0 && wi < g.W)
-                    ? __ldg(x + img * g.sx0 + c * g.sx1 + hi_ * g.sx2 + wi * g.sx3)
-                    : g.fill;
-        }
-        tile[tx][a] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-        const int a = ty + 8 * j;
-        const int64_t pp = p0 + a, k = k0 + tx;
-        if (pp < g.P && k < g.Kp) {
-            const float v = tile[a][tx];
-            const float h = rna_tf32(v);
-            hi[pp * g.Kp + k] = h;
-            lo[pp * g.Kp + k] = tf32_lo(v, h);
-        }
-    }
-}
-
-// Conv prepass: filters w[co, c, r, s] (any strides) -> hi/lo [CO][Kp]
-// filters W[co][c][r][s] -> hi/lo [co][Kp]; tap order k = (c, r, s) or, with
-// rsc, k = (r, s, c) (the TMA conv's 4-channel groups)
-__global__ void __launch_bounds__(256) filter_split_kernel(const float *__restrict__ w, int64_t CO, int64_t K,
-                                                           int64_t Kp, int64_t C, int64_t R, int64_t S,
-                                                           int64_t sw0, int64_t sw1, int64_t sw2, int64_t sw3,
-                                                           int rsc, float *__restrict__ hi,
-                                                           float *__restrict__ lo) {
-    const int64_t total = CO * Kp;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t co = e / Kp, k = e % Kp;
-        float v = 0.0f;
-        if (k < K) {
-            int64_t c, r, s;
-            if (rsc) {
-                const int64_t rs = k / C;
-                c = k % C;
-                r = rs / S;
-                s = rs % S;
-            } else {
-                const int64_t rs = R * S;
-                c = k / rs;
-                r = (k % rs) / S;
-                s = k % S;
-            }
-            v = __ldg(w + co * sw0 + c * sw1 + r * sw2 + s * sw3);
-        }
-        const float h = rna_tf32(v);
-        hi[e] = h;
-        lo[e] = tf32_lo(v, h);
     }
 }
 
@@ -893,14 +801,14 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
             }
         }
         float4 pre[BN / 128][LSB_MAX_EPI];
-        if (p.epi.n && !p.fast_n && p.conv_hw == 0) {
+        if (p.epi.n && !p.fast_n) {
 #pragma unroll
             for (int h = 0; h < BN / 128; h++) {
                 const int64_t n = n0 + (h * 32 + lane) * 4;
                 if (n < p.N) epi4_preload(p.epi, n, n + 3 < p.N, pre[h]);
             }
         }
-        if ((p.fast_n || p.epi.n == 0) && p.conv_hw == 0 && p.c_vec) {
+        if ((p.fast_n || p.epi.n == 0) && p.c_vec) {
             // no epilogue or the fast one, in its own loop: bias adds and ReLUs
             // only, no per-element dispatch on the generic stage table
             const bool b0 = p.fbias[0] != nullptr, r0 = p.frelu[0] != 0;
@@ -948,19 +856,6 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 const int64_t n = n0 + chunk * 4;
                 float x[4] = {v.x, v.y, v.z, v.w};
 
-                if (p.conv_hw > 0) {
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        const int64_t pix = n + e;
-                        if (pix >= p.N) continue;
-                        const int64_t img = pix / p.conv_hw, hw = pix % p.conv_hw;
-                        const int64_t ho = hw / p.conv_wo, wo = hw % p.conv_wo;
-                        float y = x[e];
-                        if (p.epi.n) y = apply_epilogue(p.epi, y, img, m, ho, wo);
-                        p.C[img * p.so[0] + m * p.so[1] + ho * p.so[2] + wo * p.so[3]] = y;
-                    }
-                    continue;
-                }
                 if (p.fast_n) {
 #pragma unroll
                     for (int i = 0; i < 2; i++) {

@@ -96,6 +96,7 @@ _SIGS = {
     "lsb_abi_version": ([], ctypes.c_int),
     "lsb_init": ([ctypes.c_int], ctypes.c_int),
     "lsb_last_error": ([ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
+    "lsb_reload_env": ([], ctypes.c_int),
     "lsb_device_info": ([ctypes.c_int] + [ctypes.POINTER(ctypes.c_int)] * 4, ctypes.c_int),
     "lsb_device_alloc": ([ctypes.POINTER(vp), ctypes.c_size_t], ctypes.c_int),
     "lsb_device_free": ([vp], ctypes.c_int),
@@ -178,6 +179,20 @@ def init(device: int = 0) -> None:
         return
     check(lib().lsb_init(device), f"lsb_init({device})")
     _INIT_DEVICES.add(device)
+
+
+def reload_env() -> None:
+    """Make liblsb re-read its LSB_* environment knobs (read once otherwise)."""
+    check(lib().lsb_reload_env(), "lsb_reload_env")
+
+
+def setenv(name: str, value: str | None) -> None:
+    """Set (or with None unset) an LSB_* knob and reload the library's copy."""
+    if value is None:
+        os.environ.pop(name, None)
+    else:
+        os.environ[name] = value
+    reload_env()
 
 
 def device_info(device: int = 0) -> dict:

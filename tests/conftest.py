@@ -26,3 +26,48 @@ def pytest_collection_modifyitems(config, items):
     # gpu tests fail loudly (no CPU fallback) -- never silently skip them when
     # they were selected explicitly with -m gpu
     pass
+
+
+class _KnobPatch:
+    """monkeypatch whose setenv / delenv also make liblsb re-read its LSB_*
+    knobs (the library reads the environment once, not per launch)."""
+
+    def __init__(self, mp):
+        self._mp = mp
+
+    def __getattr__(self, name):
+        return getattr(self._mp, name)
+
+    def _reload(self):
+        try:
+            from paper_2205_00618_b200 import native
+            if native._LIB is not None:
+                native.reload_env()
+        except Exception:
+            pass
+
+    def setenv(self, *a, **k):
+        self._mp.setenv(*a, **k)
+        self._reload()
+
+    def delenv(self, *a, **k):
+        self._mp.delenv(*a, **k)
+        self._reload()
+
+
+@pytest.fixture
+def monkeypatch(monkeypatch):
+    yield _KnobPatch(monkeypatch)
+
+
+@pytest.fixture(autouse=True)
+def _lsb_knobs_restored():
+    """After each test (and after monkeypatch undid its env changes) the
+    library's knob copy matches the environment again."""
+    yield
+    try:
+        from paper_2205_00618_b200 import native
+        if native._LIB is not None:
+            native.reload_env()
+    except Exception:
+        pass

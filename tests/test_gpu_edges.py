@@ -177,7 +177,7 @@ def test_tf32x3_inf_with_bias_relu_epilogue(monkeypatch):
         _same(got[s], ref[s], exact=False)
 
 
-@pytest.mark.parametrize("algo", ["simt", "tf32x3"])
+@pytest.mark.parametrize("algo", ["simt", "tf32x3", "tf32x3_nhwc", "tf32x3_planar"])
 def test_conv_nonfinite(algo, monkeypatch):
     """inf/NaN in X and W through the conv paths; on the tensor-core path the
     prepass flags them and the tile is recomputed in FP32."""
@@ -282,3 +282,49 @@ def test_tropical_underfilled_modes(mode, op, shape, monkeypatch):
     ref = O.reference_eval(gj, ins, restrict={mvar: rows})
     out = [s for s in ref][0]
     _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
+
+
+def _conv_pad1_f64(x, w):
+    n, c, h, wd = x.shape
+    xp = np.pad(x.astype(np.float64), ((0, 0), (0, 0), (1, 1), (1, 1)))
+    out = np.zeros((n, w.shape[0], h, wd))
+    for i in range(3):
+        for j in range(3):
+            out += np.einsum("nchw,oc->nohw", xp[:, :, i:i + h, j:j + wd], w[:, :, i, j].astype(np.float64),
+                             optimize=True)
+    return out
+
+
+@pytest.mark.parametrize("n,ci,hw,co", [(2, 20, 30, 70), (3, 16, 17, 64), (32, 16, 56, 64), (1, 3, 100, 8)])
+def test_planar_conv_geometries(n, ci, hw, co, monkeypatch):
+    """The planar conv (conv_planar.cuh) on pad-1 3x3 convs resized from the
+    guarded-view fixture: channels not a multiple of 16 (zero-padded block),
+    two output-channel tiles, a single image smaller than a pixel tile, and
+    32 images of 56x56 = 421 pixel tiles > 148 SMs (the stream-K path with
+    partial segments summed by the last arriver); uniform floats, strict rule
+    against f64."""
+    monkeypatch.setenv("LSB_GEMM_ALGO", "tf32x3_planar")
+    gj = _graph("conv_pad1_small", n=n, ci=ci, hp=hw, wp=hw, h=hw, w=hw, co=co)
+    k = backend.compile_graph(gj)
+    assert k.plan.steps[0].kind == "conv"
+    rng = np.random.default_rng(n * 1000 + ci)
+    x = rng.uniform(-1, 1, (n, ci, hw, hw)).astype(np.float32)
+    w = rng.normal(0, 0.1, (co, ci, 3, 3)).astype(np.float32)
+    got = _run(k, {0: x, 1: w})[2].reshape(n, co, hw, hw)
+    ref = _conv_pad1_f64(x, w)
+    ok = common.strict_ok(got, ref)
+    assert ok.all(), (float(ok.mean()), common.ref_metric(got, ref))
+
+
+def test_planar_conv_deterministic(monkeypatch):
+    """Stream-K partials are summed in segment order by whichever CTA arrives
+    last: two runs give the same bytes."""
+    monkeypatch.setenv("LSB_GEMM_ALGO", "tf32x3_planar")
+    gj = _graph("conv_pad1_small", n=32, ci=16, hp=56, wp=56, h=56, w=56, co=64)
+    k = backend.compile_graph(gj)
+    rng = np.random.default_rng(9)
+    ins = {0: rng.uniform(-1, 1, (32, 16, 56, 56)).astype(np.float32),
+           1: rng.normal(0, 0.1, (64, 16, 3, 3)).astype(np.float32)}
+    a = _run(k, ins)[2]
+    b = _run(k, ins)[2]
+    assert np.array_equal(a, b)
