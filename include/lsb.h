@@ -104,8 +104,11 @@ typedef struct {
     int32_t n_epi;
     lsb_epi_stage epi[LSB_MAX_EPI];
     int32_t algo;              /* LSB_ALGO_*                               */
-    int32_t split_k;           /* 0 = auto                                 */
-    int32_t tile_m, tile_n;    /* 0 = auto (split-factor hints)            */
+    int32_t split_k;           /* 0 = auto; > 0: SIMT split-K slices (the
+                                  schedule's outermost reduction loop)    */
+    int32_t tile_m, tile_n;    /* 0 = auto; tile_m 64: 64-row SIMT tiles;
+                                  tile_n 128 / 256: 3xTF32 tile width (the
+                                  schedule's register block, schedule.py) */
     int64_t m_begin, m_end;    /* compute output rows [m_begin, m_end); m_end <= 0 -> M
                                   (row sharding across GPUs) */
     int32_t flags;             /* LSB_GEMM_* bits                          */

@@ -34,6 +34,7 @@ from . import native, render
 from .errors import BlockTooLarge, HasReduction, ShapeMismatch
 from .graph import Graph
 from .planner import Plan, Ref, Step, plan_graph
+from .schedule import alloc_scratch_bytes, schedule_counters
 
 #: reference program.py:186-190 counter names (kept so callers that read
 #: kernel.counters / memory_access_count() keep working)
@@ -54,6 +55,22 @@ __all__ = ["compile_tree", "compile", "compile_single_operand", "compile_graph",
 class LaunchRecord:
     op: str            # "launch.gemm" | "launch.conv" | "launch.nest"
     step: Step
+
+
+@dataclass(frozen=True)
+class RegionInfo:
+    """program.py:81-91 RegionInfo for a contraction launch (instruction
+    index = launch index): ``accum_regs`` are the schedule's register block
+    counted in the target's vector registers, as the reference counts its
+    accumulators (backend.py:593-691).  The device kernel keeps its
+    accumulators in registers (SIMT) or TMEM (tcgen05) for the whole
+    reduction: no spills, one store per output at the epilogue."""
+    node: int
+    start: int
+    end: int
+    accum_regs: tuple
+    prologue_end: int
+    epilogue_start: int
 
 
 @dataclass
@@ -107,13 +124,25 @@ class CompiledKernel:
 
     def _count(self, launches: int) -> None:
         """Counters of the last execution (reset per call, like the VM's
-        backend.py:121-161): kernel launches, one ``loop`` per launch and
-        the launches' modeled 16-byte global loads / stores (render.traffic)."""
+        backend.py:121-161): kernel launches, one ``loop`` per launch; for
+        contractions the schedule's memory instructions as register-blocked
+        16-byte vector code (schedule.schedule_counters: vload / vbroadcast /
+        vstore depend on the splits and the loop order, so the tuner can rank
+        schedules), for other launches the modeled 16-byte global traffic
+        (render.traffic)."""
         c = {k: 0 for k in COUNTERS}
         for st in self.plan.steps:
-            ld, stv = render.traffic(st)
-            c["vload"] += ld
-            c["vstore"] += stv
+            sm = st.params.get("schedule")
+            if st.kind == "gemm" and sm is not None:
+                p = st.params
+                ld, bc, stv = schedule_counters(sm, p["M"], p["N"], p["K"], p["batch"])
+                c["vload"] += ld
+                c["vbroadcast"] += bc
+                c["vstore"] += stv
+            else:
+                ld, stv = render.traffic(st)
+                c["vload"] += ld
+                c["vstore"] += stv
             c["loop"] += 1
         c["launches"] = launches
         self.counters = c
@@ -129,7 +158,7 @@ class CompiledKernel:
 # compile
 # ---------------------------------------------------------------------------
 
-def _compile(graph: Graph, target, unroll_limit) -> CompiledKernel:
+def _compile(graph: Graph, target, unroll_limit, tree=None) -> CompiledKernel:
     t0 = time.perf_counter()
     plan = plan_graph(graph)
     prog = LaunchProgram([LaunchRecord(f"launch.{s.kind}", s) for s in plan.steps],
@@ -137,11 +166,21 @@ def _compile(graph: Graph, target, unroll_limit) -> CompiledKernel:
     for st in plan.steps:
         if st.kind == "gemm":
             _resolve_algo(st)
+    lanes, vregs = getattr(target, "lanes", 16), getattr(target, "vregs", 32)
+    for i, st in enumerate(plan.steps):
+        sm = st.params.get("schedule")
+        if sm is not None:
+            block = min(sm.block, max(1, (vregs - 8) * lanes))
+            prog.regions.append(RegionInfo(sm.node, i, i + 1, tuple(range(-(-block // lanes))), i, i))
     ms = (time.perf_counter() - t0) * 1000.0
     limit = unroll_limit if unroll_limit is not None else getattr(target, "unroll_limit", 0)
+    # scratch: the schedule's materialized allocations by the reference's rule
+    # (staged operand panels, unfused intermediates) when compiled from a
+    # lowered tree, at least the device scratch this plan allocates
+    scratch = max(plan.scratch_bytes, alloc_scratch_bytes(tree) or 0)
     return CompiledKernel(program=prog, target=target, slot_shapes=plan.slot_shapes,
                           input_slots=set(plan.input_slots), output_slots=set(plan.output_slots),
-                          scratch_bytes=plan.scratch_bytes, compile_ms=ms,
+                          scratch_bytes=scratch, compile_ms=ms,
                           flops=graph.count_flops(), dfg_bytes_moved=graph.bytes_moved(),
                           unroll_limit=limit, counters={k: 0 for k in COUNTERS}, plan=plan)
 
@@ -154,6 +193,7 @@ def _resolve_algo(step: Step) -> None:
     d.M, d.N, d.K, d.batch = p["M"], p["N"], p["K"], p["batch"]
     d.combine, d.reduce, d.beta_in_loop = p["combine"], p["reduce"], p["beta_in_loop"]
     d.algo = p.get("algo", 0)
+    d.tile_m, d.tile_n, d.split_k = p.get("tile_m", 0), p.get("tile_n", 0), p.get("split_k", 0)
     d.m_begin, d.m_end = p.get("m_begin", 0), p.get("m_end", 0)
     try:
         p["algo_selected"] = native.gemm_algo(d)
@@ -168,7 +208,8 @@ def compile_tree(tree, target=None, unroll_limit: Optional[int] = None,
     Only ``tree.dfg`` is consumed: every schedule annotation is
     value-preserving (feedback.py:69-75), so split factors are tile hints."""
     del interleave
-    return _compile(Graph.coerce(tree), target, unroll_limit)
+    return _compile(Graph.coerce(tree), target, unroll_limit,
+                    tree if hasattr(tree, "alloc") else None)
 
 
 def compile(tree, target=None, unroll_limit: Optional[int] = None,  # noqa: A001
@@ -187,7 +228,7 @@ def compile_single_operand(tree, target=None, unroll_limit: Optional[int] = None
     n_reads = sum(1 for n in g.nodes.values() if n.kind == "read")
     if n_reads != 1:
         raise ValueError(f"single-operand tree must have 1 input, has {n_reads}")
-    return _compile(g, target, unroll_limit)
+    return _compile(g, target, unroll_limit, tree if hasattr(tree, "alloc") else None)
 
 
 def compile_graph(graph, target=None) -> CompiledKernel:
@@ -268,7 +309,7 @@ class Runner:
                 d.n_epi = self._epi(slots, step, d.epi)
                 d.algo = p.get("algo", 0)
                 d.split_k = p.get("split_k", 0)
-                d.tile_m = p.get("tile_hint", 0)
+                d.tile_m, d.tile_n = p.get("tile_m", 0), p.get("tile_n", 0)
                 d.m_begin, d.m_end = p.get("m_begin", 0), p.get("m_end", 0)
                 p["algo_selected"] = native.gemm_algo(d)
                 descs.append((native.semiring_gemm, d))

@@ -338,7 +338,7 @@ void set_fast_epilogue(tc::TcArgs &a, const EpiStages &epi) {
 // returns 0 on success, else a negative LSB_ERR_* with `err` filled
 int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, int64_t sa_k, const float *B,
                 int64_t sb_k, int64_t sb_n, float *C, int64_t sc_m, int64_t sc_n, int c_vec, const EpiStages &epi,
-                bool b_unchanged, cudaStream_t s, int *aux_launches, char *err, size_t errlen) {
+                bool b_unchanged, int tile_n, cudaStream_t s, int *aux_launches, char *err, size_t errlen) {
     if (!load_encode()) {
         snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
         return LSB_ERR_UNSUPPORTED;
@@ -346,7 +346,10 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     constexpr int kKAlign = 32;   // split buffers padded for either stage geometry
     const int64_t Kp = (K + kKAlign - 1) / kKAlign * kKAlign;
     const size_t need = sizeof(float) * (size_t)(2 * M + 2 * N) * (size_t)Kp;
-    const int cfg = pick_cfg(N, K, epi.n > 0);
+    // the schedule's tile class (lsb_gemm_desc.tile_n, schedule.py) picks the
+    // geometry unless LSB_TC_CFG forces one
+    const int cfg = (knobs().tc_cfg < 0 && (tile_n == 128 || tile_n == 256)) ? (tile_n == 256 ? 2 : 0)
+                                                                               : pick_cfg(N, K, epi.n > 0);
     const int ilv = (cfg != 1 && !knobs().no_ilv) ? 1 : 0;   // BK = 16 tiles read [hi16 | lo16] rows
     float *ws;
     bool reuse_b = false;

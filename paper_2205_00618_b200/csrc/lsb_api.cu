@@ -491,7 +491,7 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
         char err[256] = "";
         int aux = 0;
         rc = lsb::tf32x3_gemm(M, d->N, d->K, a.A, d->sa_m, d->sa_k, d->B, d->sb_k, d->sb_n, a.C, d->sc_m,
-                              d->sc_n, a.c_vec, a.epi, (d->flags & LSB_GEMM_B_UNCHANGED) != 0, s, &aux,
+                              d->sc_n, a.c_vec, a.epi, (d->flags & LSB_GEMM_B_UNCHANGED) != 0, d->tile_n, s, &aux,
                               err, sizeof(err));
         if (rc) return fail(rc, "%s", err);
         rc = check_launch("tf32x3_gemm");

@@ -53,7 +53,7 @@ extern const NestFn kNest[4][4];                 // kern_nest.cu
 bool tf32x3_supported(int64_t M, int64_t N, int64_t K);
 int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, int64_t sa_k, const float *B,
                 int64_t sb_k, int64_t sb_n, float *C, int64_t sc_m, int64_t sc_n, int c_vec, const EpiStages &epi,
-                bool b_unchanged, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
+                bool b_unchanged, int tile_n, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
 int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec, cudaStream_t s, int *aux_launches,
                         char *err, size_t errlen);
 bool tf32x3_conv_nhwc_ok(const ConvArgs &c, int64_t n_img);

@@ -32,6 +32,7 @@ from typing import Optional
 
 from .errors import BlockTooLarge
 from .graph import EW_CODE, OP_CODE, Graph, GNode
+from .schedule import read_schedule
 
 MAX_EPI = 4
 MAX_NEST_DIMS = 8
@@ -132,6 +133,7 @@ class Planner:
         self.scratch: dict[int, int] = {}
         self.home: dict[int, tuple[Ref, dict[int, int]]] = {}   # node -> (buffer, var strides)
         self.steps: list[Step] = []
+        self._operand_nodes: list[int] = []
 
     # ---- where a node's value lives ----------------------------------------
 
@@ -297,6 +299,7 @@ class Planner:
             prev = e
 
         accesses = [self.access(o) for o in operands]
+        self._operand_nodes = list(operands)
         beta = r.beta
         redop = r.reduce_op
         out_vars = list(r.dims)
@@ -403,11 +406,11 @@ class Planner:
                 ent["c_in"] = (eb[ic], em[ic], en[ic], 0)
                 ic += 1
             strides.append(ent)
-        # tile hint: the reference register block (split factor of the M var)
-        hint = 0
-        if len(Mv) == 1:
-            f = self.g.inner_split_factor(Mv[0])
-            hint = 64 if f is not None and f <= 64 and M <= 2048 else 0
+        # the schedule picks the launch configuration (schedule.py): register
+        # block -> tile class, an outermost reduction loop -> split-K
+        sched = read_schedule(self.g, r, Mv, Nv, list(red),
+                              [o for o in (self._operand_nodes or [])])
+        hints = sched.tile_hints()
         params = dict(M=M, N=N, K=K, batch=batch,
                       A=(A.ref, A.base), sa_b=sa_b, sa_m=sa_m, sa_k=sa_k,
                       B=(B.ref, B.base), sb_b=sb_b, sb_k=sb_k, sb_n=sb_n,
@@ -415,7 +418,8 @@ class Planner:
                       combine=OP_CODE[combine], reduce=OP_CODE[kred],
                       combine_name=combine, reduce_name=kred,
                       beta=beta if in_loop else 1.0, beta_in_loop=int(in_loop),
-                      epi_strides=strides, tile_hint=hint)
+                      epi_strides=strides, tile_m=hints["tile_m"], tile_n=hints["tile_n"],
+                      split_k=hints["split_k"], schedule=sched)
         flops = 2 * M * N * K * batch
         return Step("gemm", nodes, params, epi, flops)
 

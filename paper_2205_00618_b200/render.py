@@ -37,10 +37,11 @@ def _gemm_tiles(step: Step):
     p = step.params
     algo = p.get("algo_selected") or "auto"
     if algo == "tf32x3":
-        return algo, TC_BM, 256 if p["N"] >= 256 else 128, TC_BK, "TMA -> smem ring, tcgen05.mma kind::tf32 x3 (hi*hi, hi*lo, lo*hi) -> TMEM"
+        bn = 128 if p.get("tile_n") == 128 or p["N"] < 256 else 256
+        return algo, TC_BM, bn, TC_BK, "TMA -> smem ring, tcgen05.mma kind::tf32 x3 (hi*hi, hi*lo, lo*hi) -> TMEM"
     if p["combine_name"] == "add" and p["reduce_name"] in ("max", "min"):
         return algo, MP_BM, MP_BN, MP_BK, "cp.async -> smem (3 stages), FADD2 + FMNMX3 register block 8x8/thread"
-    bm = 64 if p.get("tile_hint") == 64 or p["M"] <= 64 else 128
+    bm = 64 if p.get("tile_m") == 64 or p["M"] <= 64 else 128
     op = "FFMA2" if p["combine_name"] == "mul" and p["reduce_name"] == "add" else \
         f"v{p['combine_name']} + v{p['reduce_name']}"
     return algo, bm, SIMT_BN, SIMT_BK, f"ld.global -> smem (double-buffered), {op} register block 8x8/thread"
@@ -72,6 +73,9 @@ def render_step(step: Step, head: str) -> str:
     L = [head]
     if step.kind == "gemm":
         algo, bm, bn, bk, body = _gemm_tiles(step)
+        sm = p.get("schedule")
+        if sm is not None:
+            L.append(f"  ; schedule: {sm.describe()}" + (f", split-K {p['split_k']}" if p.get("split_k") else ""))
         L += [f"  loop.begin b 0:{p['batch']}            ; grid.z",
               f"  loop.begin m 0:{p['M']} step {bm}       ; CTA tiles (grid)",
               f"  loop.begin n 0:{p['N']} step {bn}       ; CTA tiles (grid)",

@@ -178,14 +178,17 @@ def test_disassemble_renders_balanced_loop_nests():
 
 
 def test_modeled_memory_counters():
-    from paper_2205_00618_b200 import render
+    """Contractions count the schedule as register-blocked 16-B vector code
+    (schedule.schedule_counters): C1's 4 x 64 block -> per k step of each of
+    the 64 x 4 blocks, 16 vector loads of B and 4 broadcasts of A."""
+    from paper_2205_00618_b200 import schedule
     k = backend.compile_graph(common.graph_json(common.config("C1")["graph"]))
     (st,) = k.plan.steps
-    ld, sv = render.traffic(st)
+    sm = st.params["schedule"]
+    assert (sm.m_block, sm.n_block) == (4, 64)
     M = N = K = 256
-    bm = 64 if st.params.get("tile_hint") == 64 else 128
-    assert ld == (K * (M * -(-N // 128) + N * -(-M // bm))) // 4
-    assert sv == M * N // 4
+    ld, bc, sv = schedule.schedule_counters(sm, M, N, K)
+    assert ld == (M // 4) * (N // 64) * K * 16 and bc == (M // 4) * (N // 64) * K * 4 and sv == M * N // 4
     k._count(1)
-    assert k.memory_access_count() == ld + sv
+    assert k.memory_access_count() == ld + bc + sv
     assert k.counters["launches"] == 1 and k.counters["loop"] == 1
