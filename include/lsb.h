@@ -232,6 +232,20 @@ int lsb_event_destroy(void *event);
 int lsb_event_record(void *event, void *stream);
 int lsb_stream_wait_event(void *stream, void *event);
 
+/* Copies between ordinary (pageable) host memory and the device through
+ * page-locked staging slots filled and drained by a pool of host threads
+ * (csrc/lsb_stage.cu): the DMAs run at pinned speed and overlap the host
+ * copies.  h2d returns once `src` has been read (the DMAs are enqueued on
+ * `stream`); d2h enqueues the DMAs and returns -- `dst` is complete after
+ * lsb_stage_wait().  One calling thread at a time. */
+int lsb_stage_h2d_2d(void *dst, size_t dpitch, const void *src, size_t spitch,
+                     size_t width, size_t height, void *stream);
+int lsb_stage_d2h_2d(void *dst, size_t dpitch, const void *src, size_t spitch,
+                     size_t width, size_t height, void *stream);
+int lsb_stage_wait(void);
+/* *pinned = 1 when `p` is page-locked (cudaHostAlloc'd or registered). */
+int lsb_host_is_pinned(const void *p, int *pinned);
+
 /* ---- kernels ---------------------------------------------------------------- */
 int lsb_semiring_gemm(const lsb_gemm_desc *desc, void *stream);
 /* the LSB_ALGO_* lsb_semiring_gemm will use for `desc` (AUTO resolved:

@@ -419,6 +419,44 @@ def run_device(kernel: CompiledKernel, slots: dict[int, int], stream: int = 0) -
     return kernel.runner.launch(slots, stream)
 
 
+#: host buffers at least this large that are not page-locked cross PCIe
+#: through liblsb's staging slots (lsb_stage_*: pinned ring + host copy pool);
+#: a plain pageable cudaMemcpyAsync runs at ~11 GB/s and blocks the caller
+STAGE_MIN_BYTES = 1 << 20
+
+
+def _pinned(arr) -> bool:
+    return arr.nbytes < STAGE_MIN_BYTES or native.is_pinned(arr.ctypes.data)
+
+
+def _h2d(dst: int, src: int, nbytes: int, stream: int, pinned: bool) -> None:
+    if pinned:
+        native.h2d(dst, src, nbytes, stream)
+    else:
+        native.stage_h2d_2d(dst, nbytes, src, nbytes, nbytes, 1, stream)
+
+
+def _h2d_2d(dst, dpitch, src, spitch, width, height, stream, pinned) -> None:
+    if pinned:
+        native.h2d_2d(dst, dpitch, src, spitch, width, height, stream)
+    else:
+        native.stage_h2d_2d(dst, dpitch, src, spitch, width, height, stream)
+
+
+def _d2h(dst: int, src: int, nbytes: int, stream: int, pinned: bool) -> None:
+    if pinned:
+        native.d2h(dst, src, nbytes, stream)
+    else:
+        native.stage_d2h_2d(dst, nbytes, src, nbytes, nbytes, 1, stream)
+
+
+def _d2h_2d(dst, dpitch, src, spitch, width, height, stream, pinned) -> None:
+    if pinned:
+        native.d2h_2d(dst, dpitch, src, spitch, width, height, stream)
+    else:
+        native.stage_d2h_2d(dst, dpitch, src, spitch, width, height, stream)
+
+
 def _reads_c_in(plan: Plan) -> bool:
     return any(e.c_in is not None for s in plan.steps for e in s.epi)
 
@@ -464,7 +502,7 @@ def _execute_row_streamed(kernel, r: "Runner", dev, hosts, buffers, rows) -> int
     pre = native.Event()
     for slot, host in hosts.items():
         if slot not in (a_slot, c_slot):
-            native.h2d(dev[slot], host.ctypes.data, host.nbytes, s_in.handle)
+            _h2d(dev[slot], host.ctypes.data, host.nbytes, s_in.handle, _pinned(host))
     pre.record(s_in)
     s_c.wait(pre)
     ahost = hosts[a_slot]
@@ -473,25 +511,27 @@ def _execute_row_streamed(kernel, r: "Runner", dev, hosts, buffers, rows) -> int
     direct = (dst is not None and dst.dtype == np.float32 and dst.flags.c_contiguous
               and dst.flags.writeable)
     out = dst if direct else np.empty(kernel.slot_shapes[c_slot], np.float32)
+    a_pin, c_pin, o_pin = _pinned(ahost), chost_in is None or _pinned(chost_in), _pinned(out)
     launches = 0
     events = []
     for i, (r0, r1) in enumerate(blocks):
         ein, ec = native.Event(), native.Event()
-        native.h2d(dev[a_slot] + 4 * r0 * sa_m, ahost.ctypes.data + 4 * r0 * sa_m, 4 * (r1 - r0) * sa_m,
-                   s_in.handle)
+        _h2d(dev[a_slot] + 4 * r0 * sa_m, ahost.ctypes.data + 4 * r0 * sa_m, 4 * (r1 - r0) * sa_m,
+             s_in.handle, a_pin)
         if chost_in is not None:
-            native.h2d(dev[c_slot] + 4 * r0 * sc_m, chost_in.ctypes.data + 4 * r0 * sc_m,
-                       4 * (r1 - r0) * sc_m, s_in.handle)
+            _h2d(dev[c_slot] + 4 * r0 * sc_m, chost_in.ctypes.data + 4 * r0 * sc_m,
+                 4 * (r1 - r0) * sc_m, s_in.handle, c_pin)
         ein.record(s_in)
         s_c.wait(ein)
         launches += r.launch_rows(dev, s_c.handle, r0, r1, b_unchanged=i > 0)
         ec.record(s_c)
         s_out.wait(ec)
-        native.d2h(out.ctypes.data + 4 * r0 * sc_m, dev[c_slot] + 4 * r0 * sc_m, 4 * (r1 - r0) * sc_m,
-                   s_out.handle)
+        _d2h(out.ctypes.data + 4 * r0 * sc_m, dev[c_slot] + 4 * r0 * sc_m, 4 * (r1 - r0) * sc_m,
+             s_out.handle, o_pin)
         events.append((ein, ec))
     s_out.sync()
     s_c.sync()
+    native.stage_wait()
     if not direct:
         if dst is not None:
             dst.reshape(-1)[:] = out.reshape(-1).astype(dst.dtype)
@@ -566,11 +606,12 @@ def _execute_blocked(kernel, r: "Runner", dev, hosts, buffers, bp) -> int:
     s_in, s_c, s_out = r.streams()
     for slot, host in hosts.items():
         if slot not in (a_slot, b_slot, c_slot):
-            native.h2d(dev[slot], host.ctypes.data, host.nbytes, s_in.handle)
+            _h2d(dev[slot], host.ctypes.data, host.nbytes, s_in.handle, _pinned(host))
     ahost, bhost = hosts[a_slot], hosts[b_slot]
     dst = buffers.get(c_slot)
     direct = (dst is not None and dst.dtype == np.float32 and dst.flags.c_contiguous and dst.flags.writeable)
     out = dst if direct else np.empty(kernel.slot_shapes[c_slot], np.float32)
+    a_pin, b_pin, o_pin = _pinned(ahost), _pinned(bhost), _pinned(out)
     _block_gen[0] = _block_gen[0] + 1 if _block_gen[0] < (1 << 31) - 2 else 1 << 30
     gen = _block_gen[0]
     PA, PB, PS = native.GEMM_PREP_A, native.GEMM_PREP_B, native.GEMM_PRESPLIT
@@ -579,23 +620,23 @@ def _execute_blocked(kernel, r: "Runner", dev, hosts, buffers, bp) -> int:
     nsteps = max(len(rows), len(cols))
 
     def d2h_rect(r0, r1, c0, c1):
-        native.d2h_2d(out.ctypes.data + 4 * (r0 * N + c0), 4 * N, dev[c_slot] + 4 * (r0 * N + c0), 4 * N,
-                      4 * (c1 - c0), r1 - r0, s_out.handle)
+        _d2h_2d(out.ctypes.data + 4 * (r0 * N + c0), 4 * N, dev[c_slot] + 4 * (r0 * N + c0), 4 * N,
+                4 * (c1 - c0), r1 - r0, s_out.handle, o_pin)
 
     for i in range(nsteps):
         ea, eb = native.Event(), native.Event()
         if i < len(rows):
             r0, r1 = rows[i]
-            native.h2d(dev[a_slot] + 4 * r0 * K, ahost.ctypes.data + 4 * r0 * K, 4 * (r1 - r0) * K, s_in.handle)
+            _h2d(dev[a_slot] + 4 * r0 * K, ahost.ctypes.data + 4 * r0 * K, 4 * (r1 - r0) * K, s_in.handle, a_pin)
             ea.record(s_in)
         if i < len(cols):
             c0, c1 = cols[i]
             if bp["b_rowmajor"]:
-                native.h2d_2d(dev[b_slot] + 4 * c0, 4 * N, bhost.ctypes.data + 4 * c0, 4 * N, 4 * (c1 - c0), K,
-                              s_in.handle)
+                _h2d_2d(dev[b_slot] + 4 * c0, 4 * N, bhost.ctypes.data + 4 * c0, 4 * N, 4 * (c1 - c0), K,
+                        s_in.handle, b_pin)
             else:
-                native.h2d(dev[b_slot] + 4 * c0 * K, bhost.ctypes.data + 4 * c0 * K, 4 * (c1 - c0) * K,
-                           s_in.handle)
+                _h2d(dev[b_slot] + 4 * c0 * K, bhost.ctypes.data + 4 * c0 * K, 4 * (c1 - c0) * K,
+                     s_in.handle, b_pin)
             eb.record(s_in)
         if i < len(rows):
             s_c.wait(ea)
@@ -641,6 +682,7 @@ def _execute_blocked(kernel, r: "Runner", dev, hosts, buffers, bp) -> int:
         keep += [ea, eb]
     s_out.sync()
     s_c.sync()
+    native.stage_wait()
     if not direct:
         if dst is not None:
             dst.reshape(-1)[:] = out.reshape(-1).astype(dst.dtype)
@@ -688,20 +730,22 @@ def execute(kernel: CompiledKernel, buffers: dict[int, np.ndarray]) -> None:
         return
     for slot, host in hosts.items():
         staged.append(host)
-        native.h2d(dev[slot], host.ctypes.data, host.nbytes, stream)
+        _h2d(dev[slot], host.ctypes.data, host.nbytes, stream, _pinned(host))
     launches = r.launch(dev, stream)
     outs = {}
     for slot in kernel.output_slots:
         dst = buffers.get(slot)
         if (dst is not None and dst.dtype == np.float32 and dst.flags.c_contiguous
                 and dst.flags.writeable):
-            # straight into the caller's array (pinned arrays get full DMA speed)
-            native.d2h(dst.ctypes.data, dev[slot], dst.nbytes, stream)
+            # straight into the caller's array (pinned: one DMA; pageable:
+            # through the staging slots)
+            _d2h(dst.ctypes.data, dev[slot], dst.nbytes, stream, _pinned(dst))
             continue
         res = np.empty(kernel.slot_shapes[slot], np.float32)
-        native.d2h(res.ctypes.data, dev[slot], res.nbytes, stream)
+        _d2h(res.ctypes.data, dev[slot], res.nbytes, stream, _pinned(res))
         outs[slot] = res
     native.sync(stream)
+    native.stage_wait()
     del staged
     kernel._count(launches)
     for slot, res in outs.items():

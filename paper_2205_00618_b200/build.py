@@ -28,7 +28,7 @@ LIB = os.path.join(PKG, "liblsb.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-Xptxas", "-warn-spills"]
-UNITS = ["lsb_api.cu", "kern_fast.cu", "kern_generic.cu", "kern_nest.cu", "kern_tf32.cu"]
+UNITS = ["lsb_api.cu", "lsb_stage.cu", "kern_fast.cu", "kern_generic.cu", "kern_nest.cu", "kern_tf32.cu"]
 
 
 def nvcc() -> str:
@@ -83,7 +83,7 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
         raise RuntimeError(f"nvcc failed for {failed}")
     objs = [os.path.join(OBJ, u.replace(".cu", ".o")) for u in UNITS]
     if force or jobs or _stale(LIB, objs):
-        cmd = [cc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"]
+        cmd = [cc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             sys.stderr.write(r.stdout + r.stderr)

@@ -64,6 +64,8 @@ int check_device() {
 
 int lsb::device_sms() { return sm_count(); }
 
+int lsb::report_error(int code, const char *msg) { return fail(code, "%s", msg); }
+
 namespace {
 lsb::Knobs g_knobs;
 std::once_flag g_knobs_once;

@@ -13,6 +13,7 @@ using SplitFn = void (*)(const GemmArgs &, int64_t, cudaStream_t);
 using NestFn = void (*)(const NestArgs &, cudaStream_t);
 
 int device_sms();                               // lsb_api.cu
+int report_error(int code, const char *msg);    // lsb_api.cu: sets lsb_last_error
 
 // Environment knobs, read once -- at the first use or on
 // lsb_reload_env() -- never on the launch path.  Defaults are the measured best.

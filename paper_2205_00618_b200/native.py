@@ -110,6 +110,12 @@ _SIGS = {
     "lsb_memcpy_d2h_2d": ([vp, ctypes.c_size_t, vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, vp],
                           ctypes.c_int),
     "lsb_stream_sync": ([vp], ctypes.c_int),
+    "lsb_stage_h2d_2d": ([vp, ctypes.c_size_t, vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, vp],
+                         ctypes.c_int),
+    "lsb_stage_d2h_2d": ([vp, ctypes.c_size_t, vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t, vp],
+                         ctypes.c_int),
+    "lsb_stage_wait": ([], ctypes.c_int),
+    "lsb_host_is_pinned": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "lsb_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
     "lsb_nccl_init": ([ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)], ctypes.c_int),
     "lsb_nccl_destroy": ([vp], ctypes.c_int),
@@ -279,6 +285,24 @@ def d2h_2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int
 
 def d2h(dst: int, src: int, nbytes: int, stream: int = 0) -> None:
     check(lib().lsb_memcpy_d2h(vp(dst), vp(src), nbytes, vp(stream)), "lsb_memcpy_d2h")
+
+
+def stage_h2d_2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int, stream: int = 0) -> None:
+    check(lib().lsb_stage_h2d_2d(vp(dst), dpitch, vp(src), spitch, width, height, vp(stream)), "lsb_stage_h2d_2d")
+
+
+def stage_d2h_2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int, stream: int = 0) -> None:
+    check(lib().lsb_stage_d2h_2d(vp(dst), dpitch, vp(src), spitch, width, height, vp(stream)), "lsb_stage_d2h_2d")
+
+
+def stage_wait() -> None:
+    check(lib().lsb_stage_wait(), "lsb_stage_wait")
+
+
+def is_pinned(ptr: int) -> bool:
+    v = ctypes.c_int()
+    check(lib().lsb_host_is_pinned(vp(ptr), ctypes.byref(v)), "lsb_host_is_pinned")
+    return bool(v.value)
 
 
 def d2d(dst: int, src: int, nbytes: int, stream: int = 0) -> None:
