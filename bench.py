@@ -526,7 +526,8 @@ def traffic_of(name: str, steps) -> float | None:
             t = json.load(f)
     except Exception:
         return None
-    algo = "tf32x3" if any("tf32x3" in s for s in steps) else "simt"
+    algo = "tf32x3" if any("tf32x3" in s for s in steps) else "conv" if any(s.startswith("conv") for s in steps) \
+        else "simt"
     ent = t.get(f"{name}_{algo}")
     return ent["dram_bytes_per_launch"] if ent else None
 

@@ -13,7 +13,7 @@ for r in rows[1:]:
         v = float(r[vi].replace(",", ""))
     except ValueError:
         continue
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
     acc[r[ki].split("(")[0][:60]].append(v * scale)
 for k, v in acc.items():
     print(f"{k:60s} n={len(v):3d} mean {sum(v) / len(v):9.2f} us  min {min(v):9.2f}")
