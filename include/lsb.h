@@ -245,6 +245,10 @@ int lsb_stage_d2h_2d(void *dst, size_t dpitch, const void *src, size_t spitch,
 int lsb_stage_wait(void);
 /* *pinned = 1 when `p` is page-locked (cudaHostAlloc'd or registered). */
 int lsb_host_is_pinned(const void *p, int *pinned);
+/* Geometry of the last 3xTF32 GEMM launch on this process: tile width (128 /
+ * 256), grid size, persistent units (0 = one tile per CTA), 2-CTA clusters.
+ * Diagnostics for tests and tools. */
+int lsb_last_gemm_launch(int *bn, int *ctas, int *units, int *pair);
 
 /* ---- kernels ---------------------------------------------------------------- */
 int lsb_semiring_gemm(const lsb_gemm_desc *desc, void *stream);

@@ -20,6 +20,11 @@ namespace lsb {
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+// geometry of the last tf32x3 GEMM launch (lsb_last_gemm_launch: tests)
+struct LastGemm {
+    int bn, ctas, units, pair;
+};
+LastGemm g_last_gemm = {0, 0, 0, 0};
 std::mutex g_tc_mu;
 float *g_split = nullptr;
 size_t g_split_bytes = 0;
@@ -216,15 +221,6 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
     const int units = a.m_tiles * a.n_tiles + a.m_tiles2 * a.n_tiles2 + a.split_tiles;
     int ctas = units;
     a.units = 0;
-    if (kCanPersist && (a.fast_n || a.epi.n == 0) && !knobs().no_persist) {
-        int slots = lsb::device_sms() * Cf::kCtasPerSm;
-        if (a.pair) slots &= ~1;
-        if (units > slots) {
-            a.units = units;
-            ctas = slots;
-        }
-    }
-    const size_t smem_bytes = a.units ? Cf::kSmemBytesPersist : Cf::kSmemBytes;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(tc::tf32x3_gemm_kernel<BK, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -234,6 +230,43 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
                                  (int)Cf::kSmemBytesPersist);
         attr = true;
     }
+    if (kCanPersist && (a.fast_n || a.epi.n == 0) && !knobs().no_persist) {
+        int slots = lsb::device_sms() * Cf::kCtasPerSm;
+        if (a.pair) {
+            // 2-CTA clusters: as many as the GPC layout keeps resident at once
+            // (a second wave of persistent CTAs would each walk extra units)
+            static int pair_slots = -1;
+            if (pair_slots < 0) {
+                cudaLaunchConfig_t oc = {};
+                oc.gridDim = dim3((unsigned)slots);
+                oc.blockDim = dim3(Cf::kThreads);
+                oc.dynamicSmemBytes = Cf::kSmemBytesPersist;
+                cudaLaunchAttribute oa[1];
+                oa[0].id = cudaLaunchAttributeClusterDimension;
+                oa[0].val.clusterDim.x = 2;
+                oa[0].val.clusterDim.y = 1;
+                oa[0].val.clusterDim.z = 1;
+                oc.attrs = oa;
+                oc.numAttrs = 1;
+                int clusters = 0;
+                if constexpr (kCanPersist) {
+                    if (cudaOccupancyMaxActiveClusters(&clusters, tc::tf32x3_gemm_kernel<BK, BN, true>, &oc) !=
+                        cudaSuccess) {
+                        cudaGetLastError();
+                        clusters = 0;
+                    }
+                }
+                pair_slots = clusters > 0 ? std::min(slots & ~1, 2 * clusters) : (slots & ~1);
+            }
+            slots = pair_slots;
+        }
+        if (units > slots) {
+            a.units = units;
+            ctas = slots;
+        }
+    }
+    g_last_gemm = LastGemm{BN, ctas, a.units, a.pair};
+    const size_t smem_bytes = a.units ? Cf::kSmemBytesPersist : Cf::kSmemBytes;
     dim3 grid((unsigned)ctas);
     static long long *trace = nullptr;
     const char *trace_path = knobs().gemm_trace[0] ? knobs().gemm_trace : nullptr;
@@ -876,3 +909,11 @@ int conv_planar(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launc
 }
 
 }  // namespace lsb
+
+extern "C" int lsb_last_gemm_launch(int *bn, int *ctas, int *units, int *pair) {
+    if (bn) *bn = lsb::g_last_gemm.bn;
+    if (ctas) *ctas = lsb::g_last_gemm.ctas;
+    if (units) *units = lsb::g_last_gemm.units;
+    if (pair) *pair = lsb::g_last_gemm.pair;
+    return 0;
+}

@@ -116,6 +116,7 @@ _SIGS = {
                          ctypes.c_int),
     "lsb_stage_wait": ([], ctypes.c_int),
     "lsb_host_is_pinned": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "lsb_last_gemm_launch": ([ctypes.POINTER(ctypes.c_int)] * 4, ctypes.c_int),
     "lsb_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
     "lsb_nccl_init": ([ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)], ctypes.c_int),
     "lsb_nccl_destroy": ([vp], ctypes.c_int),
@@ -303,6 +304,14 @@ def is_pinned(ptr: int) -> bool:
     v = ctypes.c_int()
     check(lib().lsb_host_is_pinned(vp(ptr), ctypes.byref(v)), "lsb_host_is_pinned")
     return bool(v.value)
+
+
+def last_gemm_launch() -> dict:
+    """Geometry of the last 3xTF32 GEMM launch (tile width, grid, persistent
+    units, 2-CTA clusters)."""
+    v = [ctypes.c_int() for _ in range(4)]
+    check(lib().lsb_last_gemm_launch(*(ctypes.byref(x) for x in v)), "lsb_last_gemm_launch")
+    return dict(zip(("bn", "ctas", "units", "pair"), (x.value for x in v)))
 
 
 def d2d(dst: int, src: int, nbytes: int, stream: int = 0) -> None:

@@ -9,13 +9,17 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
+from paper_2205_00618_b200 import native
 from test_gpu_edges import _graph, _inputs, _run, _same
 
 pytestmark = pytest.mark.gpu
 
 # (m, k, n): 4096x4096 = 512 tiles -> 444 whole + 68 split tiles (C4's layout);
-# ragged m/n with partial last tiles; one K chunk (no split: chunks < 2)
-SHAPES = [(4096, 200, 4096), (1000, 300, 4100), (2050, 70, 3000), (1536, 64, 6144)]
+# ragged m/n with partial last tiles and an even m-tile count (the 2-CTA
+# cluster path: 16 x 17 = 272 tiles); 17 x 12 tiles, odd m-tiles (no pairs);
+# one K chunk (no split: chunks < 2).  Every shape has more tiles than SMs,
+# so the persistent instance runs (asserted through lsb_last_gemm_launch).
+SHAPES = [(4096, 200, 4096), (2000, 300, 4100), (2050, 70, 3000), (1536, 64, 6144)]
 
 
 @pytest.mark.parametrize("m,k,n", SHAPES, ids=lambda v: str(v))
@@ -25,6 +29,9 @@ def test_persistent_gemm_matches_oracle_and_single_unit(m, k, n, monkeypatch):
     gj = _graph("semiring_mul_add", m=m, k=k, n=n)
     kern, ins = _inputs(gj, m * 131 + k * 7 + n)
     got = _run(kern, ins)
+    launch = native.last_gemm_launch()
+    assert launch["bn"] == 256 and launch["units"] > launch["ctas"] > 0, launch
+    assert launch["pair"] == (1 if -(-m // 128) % 2 == 0 else 0), launch
     out = next(s for s in got if s not in ins)
     mvar = [v["id"] for v in json.loads(gj)["vars"] if v["name"] == "m"][0]
     rows = np.unique(np.array([0, 127, 128, m // 2, m - 129, m - 1]).clip(0, m - 1))
@@ -32,6 +39,7 @@ def test_persistent_gemm_matches_oracle_and_single_unit(m, k, n, monkeypatch):
     _same(got[out].reshape(m, n)[rows], ref[next(iter(ref))], exact=True)
     monkeypatch.setenv("LSB_NO_PERSIST", "1")
     single = _run(kern, ins)
+    assert native.last_gemm_launch()["units"] == 0
     assert np.array_equal(got[out].view(np.uint32), single[out].view(np.uint32))
 
 
