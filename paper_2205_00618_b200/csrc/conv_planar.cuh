@@ -504,7 +504,6 @@ __global__ void __launch_bounds__(CP_THREADS, 1) conv_planar_kernel(const __grid
         const int q = warp & 3;                    // TMEM lane quadrant (warp id % 4)
         const int h = ew >> 2;                     // column half
         const bool odd = lane & 1;
-        const int co_l = 16 * q + (lane >> 1);     // output channel of this lane (after the pair sum)
         constexpr int kParts = NT / 64;            // 32-column parts per warp (NT / 2 columns)
         float acc[kParts][16];
 #pragma unroll
