@@ -719,18 +719,18 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
 }  // namespace lsb
 
 namespace lsb {
-
 // ---------------------------------------------------------------- planar conv
-// (conv_planar.cuh): stride 1, zero fill, any padding / dilation / strides of
-// X, W and O; one filter-image prepass + one persistent stream-K launch.
+// (conv_planar.cuh): stride 1, zero fill, any padding / dilation, X with a
+// unit column stride and 16-B aligned row / channel / image strides (the raw
+// X boxes are TMA loads of the original tensor); any W and O strides.  One
+// filter-image prepass + one persistent stream-K launch (programmatic
+// dependent launch: the conv's X loads overlap the prepass).
 namespace {
 std::mutex g_cp_mu;
 float *g_cp_img = nullptr, *g_cp_part = nullptr;
 size_t g_cp_img_n = 0, g_cp_part_n = 0;
 int *g_cp_flags = nullptr, *g_cp_tileflag = nullptr;   // per-tile arrival counters | [wflag, tileflag...]
 int64_t g_cp_flags_n = 0, g_cp_tileflag_n = 0;
-int *g_cp_bar = nullptr;      // grid barrier of the in-kernel filter-image build
-int64_t g_cp_bar_count = 0;   // its value after the last enqueued launch
 
 template <class T>
 bool cp_grow(T **buf, size_t *have, size_t need, bool zero, cudaStream_t s) {
@@ -747,36 +747,66 @@ bool cp_grow(T **buf, size_t *have, size_t need, bool zero, cudaStream_t s) {
     return true;
 }
 
+// X strides for the TMA map (row, channel, image); an extent-1 dimension's
+// stride is never used, so it takes a dense value the map accepts
+void cp_x_strides(const ConvArgs &c, int64_t n_img, int64_t (&sx)[3]) {
+    sx[0] = c.H > 1 ? c.sx2 : (c.W + 3) / 4 * 4;
+    sx[1] = c.C > 1 ? c.sx1 : sx[0] * c.H;
+    sx[2] = n_img > 1 ? c.sx0 : sx[1] * c.C;
+}
+
 struct CpGeom {
-    int Hp, Wp, nt, halo, tiles, co_tiles, cbs, stages;
+    int Hp, Wp, nt, halo, tpi, rb, wb, wsh, tiles, co_tiles, cbs, stages;
     int64_t units;
 };
 
 bool cp_geom(const ConvArgs &c, int64_t n_img, CpGeom &g) {
     if (c.fill != 0.0f || c.stride_h != 1 || c.stride_w != 1 || c.dil_h < 1 || c.dil_w < 1) return false;
+    // raw X boxes: TMA of the original NCHW tensor (unit column stride,
+    // 16-B aligned base and strides, 32-bit coordinates)
+    int64_t sx[3];
+    cp_x_strides(c, n_img, sx);
+    if ((c.sx3 != 1 && c.W > 1) || sx[0] % 4 || sx[1] % 4 || sx[2] % 4 || reinterpret_cast<uintptr_t>(c.x) % 16 ||
+        sx[0] <= 0 || sx[1] <= 0 || sx[2] <= 0 || sx[0] >= (1ll << 37) || sx[1] >= (1ll << 37) || sx[2] >= (1ll << 37))
+        return false;
+    if (c.H > (1 << 20) || c.W > (1 << 20) || n_img > (1 << 20)) return false;
     const int64_t Hp = c.HO + (c.R - 1) * c.dil_h, Wp = c.WO + (c.S - 1) * c.dil_w;
-    const int64_t nflat = n_img * Hp * Wp;
-    if (Hp < 1 || Wp < 1 || nflat >= (1ll << 30) || c.C > (1 << 20) || c.M > (1 << 20)) return false;
+    if (Hp < 1 || Wp < 1 || c.HO < 1 || c.WO < 1 || c.C > (1 << 20) || c.M > (1 << 20)) return false;
+    if (c.pad_w >= (1 << 15) || c.pad_h >= (1 << 15)) return false;
+    // raw box columns from w = -roundup(pw, 4): a TMA box's innermost start
+    // coordinate must be 16-B aligned
+    const int64_t wsh = (c.pad_w + 3) / 4 * 4 - c.pad_w, wb = (Wp + wsh + 3) / 4 * 4;
+    if (wb > 256) return false;
     const int64_t reach = (c.R - 1) * c.dil_h * Wp + (c.S - 1) * c.dil_w;
+    const int64_t flat = c.HO * Wp;   // per-image flat positions computed
     // pixel tile NT (the MMA's N, a multiple of 64): the smallest of 128 / 192
     // / 256 whose tile count fits one CTA per SM (whole tiles per CTA, no
-    // stream-K partials: C3 -> 192, 141 tiles), else 256; and the halo must fit
+    // stream-K partials: C3 -> 192, 8 x 17 = 136 tiles), else the largest that
+    // fits; the halo and its raw box must fit their buffers
     const int64_t sms = device_sms(), co_tiles = (c.M + 63) / 64;
     g.nt = 0;
     for (int nt : {128, 192, 256}) {
-        if (nt + reach > tc::CP_HALO) break;
+        if (knobs().cp_nt > 0 && nt != knobs().cp_nt) continue;   // experiments (LSB_CP_NT)
+        const int64_t halo = nt + reach, rb = (Wp - 1 + halo - 1) / Wp + 1;
+        if (halo > tc::CP_HALO || rb > 256 || 16 * rb * wb * 4 > tc::CP_RAW_BYTES) break;
         g.nt = nt;
-        if (co_tiles * ((nflat + nt - 1) / nt) <= sms) break;
+        if (co_tiles * n_img * ((flat + nt - 1) / nt) <= sms) break;
     }
     if (!g.nt) return false;
     g.Hp = (int)Hp;
     g.Wp = (int)Wp;
     g.halo = (int)(g.nt + reach);
-    g.tiles = (int)((nflat + g.nt - 1) / g.nt);
-    g.co_tiles = (int)((c.M + 63) / 64);
+    g.rb = (int)((Wp - 1 + g.halo - 1) / Wp + 1);
+    g.wb = (int)wb;
+    g.wsh = (int)wsh;
+    g.tpi = (int)((flat + g.nt - 1) / g.nt);
+    const int64_t tiles = n_img * g.tpi;
+    g.co_tiles = (int)co_tiles;
     g.cbs = (int)((c.C + 15) / 16);
     g.stages = g.cbs * (int)(c.R * c.S);
-    g.units = (int64_t)g.co_tiles * g.tiles * g.stages;
+    g.units = co_tiles * tiles * g.stages;
+    if (tiles >= (1 << 30) || g.units >= (1ll << 31) || co_tiles * g.stages * 1024 >= (1ll << 31)) return false;
+    g.tiles = (int)tiles;
     return load_encode() || true;
 }
 }  // namespace
@@ -789,8 +819,13 @@ bool conv_planar_ok(const ConvArgs &c, int64_t n_img) {
 int conv_planar(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen) {
     CpGeom g;
     if (!cp_geom(c, n_img, g)) {
-        snprintf(err, errlen, "planar conv needs stride 1, a 0 fill and a halo <= %d rows", tc::CP_HALO);
+        snprintf(err, errlen, "planar conv needs stride 1, a 0 fill, TMA-able X strides and a halo <= %d rows",
+                 tc::CP_HALO);
         return LSB_ERR_UNSUPPORTED;
+    }
+    if (!load_encode()) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
+        return LSB_ERR_CUDA;
     }
     // whole tiles per CTA when they fit one wave, else stream-K over every SM
     const int64_t whole = (int64_t)g.co_tiles * g.tiles;
@@ -816,31 +851,32 @@ int conv_planar(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launc
         }
         a.gen = ++g_gen;
         if (a.gen <= 0) a.gen = g_gen = 1;
-        if (!g_cp_bar && cudaMalloc(&g_cp_bar, sizeof(int)) == cudaSuccess) {
-            cudaMemsetAsync(g_cp_bar, 0, sizeof(int), s);
-            g_cp_bar_count = 0;
+    }
+    CUtensorMap mx;
+    {
+        // X[n][c][h][w] as 4-D (w, h, c, n); box = wb columns x rb rows x 16 channels
+        cuuint64_t dims[4] = {(cuuint64_t)c.W, (cuuint64_t)c.H, (cuuint64_t)c.C, (cuuint64_t)n_img};
+        int64_t sx[3];
+        cp_x_strides(c, n_img, sx);
+        cuuint64_t strides[3] = {(cuuint64_t)sx[0] * 4, (cuuint64_t)sx[1] * 4, (cuuint64_t)sx[2] * 4};
+        cuuint32_t box[4] = {(cuuint32_t)g.wb, (cuuint32_t)g.rb, 16, 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = g_encode(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(c.x), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            snprintf(err, errlen, "cuTensorMapEncodeTiled failed (planar conv X, %d)", (int)r);
+            return LSB_ERR_CUDA;
         }
-        if (!g_cp_bar) {
-            snprintf(err, errlen, "cudaMalloc of the planar conv barrier failed");
-            return LSB_ERR_NOMEM;
-        }
-        if (g_cp_bar_count > (1 << 30)) {   // re-zero long before the counter wraps
-            cudaMemsetAsync(g_cp_bar, 0, sizeof(int), s);
-            g_cp_bar_count = 0;
-        }
-        g_cp_bar_count += ctas;
-        a.gridbar = g_cp_bar;
-        a.bar_target = (int)g_cp_bar_count;
     }
     a.x = c.x;
     a.sx[0] = c.sx0; a.sx[1] = c.sx1; a.sx[2] = c.sx2; a.sx[3] = c.sx3;
     a.N = (int)n_img; a.C = (int)c.C; a.H = (int)c.H; a.W = (int)c.W; a.CO = (int)c.M;
     a.R = (int)c.R; a.S = (int)c.S; a.HO = (int)c.HO; a.WO = (int)c.WO;
     a.ph = (int)c.pad_h; a.pw = (int)c.pad_w; a.dh = (int)c.dil_h; a.dw = (int)c.dil_w;
-    a.Hp = g.Hp; a.Wp = g.Wp; a.halo = g.halo;
+    a.Hp = g.Hp; a.Wp = g.Wp; a.halo = g.halo; a.tpi = g.tpi; a.rb = g.rb; a.wb = g.wb; a.wsh = g.wsh;
     a.tiles = g.tiles; a.co_tiles = g.co_tiles; a.cbs = g.cbs; a.stages = g.stages; a.units = g.units;
     a.wimg = g_cp_img;
-    a.wimg_w = g_cp_img;
     a.o = c.o;
     a.so[0] = c.so0; a.so[1] = c.so1; a.so[2] = c.so2; a.so[3] = c.so3;
     a.part = g_cp_part;
@@ -851,7 +887,20 @@ int conv_planar(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launc
     a.swt[0] = c.sw0; a.swt[1] = c.sw1; a.swt[2] = c.sw2; a.swt[3] = c.sw3;
     a.epi = c.epi;
     a.dbg = knobs().cp_dbg;
-    if (aux_launches) *aux_launches = 0;
+    // the filter stage images (tiny; the conv's programmatic launch overlaps it)
+    {
+        tc::CpFilterArgs f;
+        f.w = c.w;
+        f.swt[0] = c.sw0; f.swt[1] = c.sw1; f.swt[2] = c.sw2; f.swt[3] = c.sw3;
+        f.CO = (int)c.M; f.C = (int)c.C; f.R = (int)c.R; f.S = (int)c.S;
+        f.stages = g.stages;
+        f.total = g.co_tiles * g.stages * 1024;
+        f.img = g_cp_img;
+        f.wflag = a.wflag;
+        f.gen = a.gen;
+        tc::cp_filter_kernel<<<(unsigned)((f.total + 255) / 256), 256, 0, s>>>(f);
+        if (aux_launches) *aux_launches = 1;
+    }
     static bool attr[3] = {false, false, false};
     const int which = g.nt == 256 ? 2 : g.nt == 192 ? 1 : 0;
     const void *kfn = which == 2 ? (const void *)tc::conv_planar_kernel<256>
@@ -875,11 +924,11 @@ int conv_planar(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launc
     cfg.dynamicSmemBytes = tc::CP_SMEM;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;   // the filter-image grid barrier: all CTAs resident
-    at[0].val.cooperative = 1;
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = (knobs().cp_dbg & 512) ? 0 : 1;   // experiments: plain launch
-    void *args[] = {&a};
+    cfg.numAttrs = (trace_path || (knobs().cp_dbg & 512)) ? 0 : 1;   // traces / experiments: plain launch
+    void *args[] = {&mx, &a};
     cudaError_t e = cudaLaunchKernelExC(&cfg, kfn, args);
     prof_mark(1, s);
     if (e != cudaSuccess) {

@@ -99,6 +99,7 @@ void read_knobs(lsb::Knobs &k) {
     k.conv_splits = num("LSB_CONV_SPLITS");
     k.cp_dbg = num("LSB_CP_DBG");
     k.cp_ctas = num("LSB_CP_CTAS");
+    k.cp_nt = num("LSB_CP_NT");
     k.scalar_split = on("LSB_SCALAR_SPLIT");
     k.no_pair = on("LSB_NO_PAIR");
     k.no_tail_split = on("LSB_NO_TAIL_SPLIT");
@@ -688,20 +689,19 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     const bool wcontig = d->sw[3] == 1 && d->sw[2] == d->S && d->sw[1] == d->R * d->S;
     a.a_mode = (wcontig && aligned16(d->w) && d->sw[0] % 4 == 0 && K % 4 == 0) ? lsb::LD_VEC_K : lsb::LD_GENERIC;
 
-    // tensor cores (split TF32) for real work: the NHWC-copy kernel
-    // (tf32x3_conv_nhwc.cuh: zero fill, strides <= 8) or the planar
-    // single-launch kernel (conv_planar.cuh: stride 1, zero fill); SIMT
-    // otherwise (nonzero fill, tiny convs).
-    // LSB_GEMM_ALGO=simt|tf32x3|tf32x3_nhwc|tf32x3_planar.
-    // Measured on C3 (tools/bench_c3.py, L2 flushed): NHWC-copy
-    // 26.7 us per step, planar 27.6 us -- the NHWC kernel first, the planar
-    // one for stride-1 convs the NHWC kernel cannot take (N*H > 65535).
+    // tensor cores (split TF32) for real work: the planar kernel
+    // (conv_planar.cuh: stride 1, zero fill, TMA-able X strides; raw X boxes
+    // converted in shared memory, no X copy), else the NHWC-copy kernel
+    // (tf32x3_conv_nhwc.cuh: zero fill, strides <= 8); SIMT otherwise
+    // (nonzero fill, tiny convs).  LSB_GEMM_ALGO=simt|tf32x3|tf32x3_nhwc|tf32x3_planar.
+    // Measured on C3 (tools/c3_probe.py, back-to-back launches):
+    // planar 21.6 us per call (filter prepass + conv), NHWC-copy 23.1 us.
     const bool big = 2.0 * a.M * a.N * d->N * K >= (double)(1ll << 28) && a.M >= 16;
     const bool planar_ok = lsb::conv_planar_ok(a, d->N), nhwc_ok = lsb::tf32x3_conv_nhwc_ok(a, d->N);
-    int tc_mode = !big ? 0 : nhwc_ok ? 4 : planar_ok ? 5 : 0;
+    int tc_mode = !big ? 0 : planar_ok ? 5 : nhwc_ok ? 4 : 0;
     switch (lsb::knobs().gemm_algo) {
     case LSB_ALGO_SIMT: tc_mode = 0; break;
-    case LSB_ALGO_TF32X3: tc_mode = nhwc_ok ? 4 : planar_ok ? 5 : 0; break;
+    case LSB_ALGO_TF32X3: tc_mode = planar_ok ? 5 : nhwc_ok ? 4 : 0; break;
     case lsb::kAlgoTf32x3Nhwc: tc_mode = nhwc_ok ? 4 : planar_ok ? 5 : 0; break;
     case lsb::kAlgoTf32x3Planar: tc_mode = planar_ok ? 5 : nhwc_ok ? 4 : 0; break;
     default: break;

@@ -26,6 +26,7 @@ struct Knobs {
     int fixup_ctas, mp_cluster, streamk_ctas, conv_splits;   // 0 = model's choice
     int cp_dbg;           // LSB_CP_DBG: planar conv timing experiments (conv_planar.cuh)
     int cp_ctas;          // LSB_CP_CTAS: planar conv grid size (0 = one CTA per SM)
+    int cp_nt;            // LSB_CP_NT: planar conv pixel tile (128 / 192 / 256; 0 = by tile count)
     bool scalar_split, no_pair, no_tail_split, no_persist, no_fast_epi, no_ilv;
     bool no_small, no_streamk, no_mp_fast, no_mp_cluster, no_conv_split;
     char gemm_trace[256], conv_trace[256];   // "" = off

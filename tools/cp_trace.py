@@ -16,7 +16,13 @@ with open(sys.argv[1]) as f:
         else:
             rows.append([int(x) for x in line.split()])
 a = np.array(rows, dtype=np.float64)
+a_raw = a.copy()
 g0, g1 = a[:, 62].copy(), a[:, 61].copy()
+if (a[:, 60] > 0).all():
+    ent, st0, ex = a[:, 60], a[:, 0], a[:, 63]
+    mhz = (ex - ent) / (g1 - g0) * 1e3
+    print("entry->start(slot 0) cycles: min %d med %d max %d | entry->exit cycles med %d | SM clock %.0f MHz (med)" % (
+        (st0 - ent).min(), np.median(st0 - ent), (st0 - ent).max(), np.median(ex - ent), np.median(mhz)))
 if (g0 > 0).all():
     t0 = g0.min()
     print("globaltimer (us): CTA start min %.2f max %.2f | end min %.2f med %.2f max %.2f" % (
@@ -30,15 +36,19 @@ for b in list(range(0, 4)) + [int(np.nanargmax(a[:, 63]))]:
     r = a[b]
     f = lambda sl: " ".join("%.1f" % x for x in r[sl] if not np.isnan(x))
     print(f"cta {b}: start {r[0]:.2f} | conv {f(slice(16, 31))} | mma {f(slice(1, 16))} | fold {f(slice(31, 46))}"
-          f" | pub {r[46]:.2f} | seg(wait0,wait1,store) {f(slice(47, 59))} | exit {r[63]:.2f}")
+          f" | raw-in {f(slice(50, 56))} | mma-go {f(slice(56, 60))} | store-end {r[49]:.2f} | exit {r[63]:.2f}")
 if srows:
     sa = np.array(srows, dtype=np.float64)
     for b in (0, 1):
-        pre, post = sa[b, 0::2], sa[b, 1::2]
-        m = post > 0
-        base = pre[m][0]
-        print(f"cta {b} stage clocks (cycles from first): wait-start", " ".join("%d" % (x - base) for x in pre[m]))
-        print(f"cta {b}                                    waited    ", " ".join("%d" % x for x in (post - pre)[m]))
-        jb = sa[b, 100:127].reshape(9, 3)
-        print(f"cta {b} job starts (halo wait, c_empty wait, go):", "; ".join(
-            "%d %d %d" % tuple(x - base for x in r) for r in jb if r[0] > 0))
+        base = a_raw[b, 0]
+        for job in range(4):
+            cells = []
+            for w in range(4):
+                ev = sa[b, 32 * job + 8 * w: 32 * job + 8 * w + 4]
+                cells.append("/".join("%.2f" % ((x - base) / 1e3) if x > 0 else "-" for x in ev))
+            print(f"cta {b} job {job} converter warps (raw-in/halo-free/converted/bar, k-cycles):", "  ".join(cells))
+            m = sa[b, 32 * job + 4: 32 * job + 7]
+            if job == 3:
+                print(f"cta {b} epilogue tail (stores start):", "%.2f" % ((sa[b, 124] - base) / 1e3))
+            print(f"cta {b} job {job} mma warp (start, halo_full passed, c_empty passed):",
+                  " ".join("%.2f" % ((x - base) / 1e3) for x in m))
