@@ -22,20 +22,26 @@
 // MMAs of the jobs in between.
 //
 // Planar operands.  Converter warps turn a raw slot into the halo as K-major
-// SWIZZLE_NONE "planes": plane g holds channels 4g..4g+3 of every halo row,
-// rows 16 B apart ([plane][row][4]), so core matrices (8 rows x 16 B) are
+// SWIZZLE_NONE "planes": fp32 plane g (0-3) holds channels 4g..4g+3 of every
+// halo row, bf16 plane 4 + g (g = 0, 1) the lo parts of channels 8g..8g+7,
+// rows 16 B apart ([plane][row][16 B]), so core matrices (8 rows x 16 B) are
 // contiguous for ANY start row: descriptor LBO = plane stride, SBO = 128 B,
 // and the tap shift is just start + off * 16 B (verified on B200:
 // tools/umma_planar_probe.cu; 128 cycles per 128x256x8 MMA, the same as the
 // swizzled layouts).
 //
-// Split TF32.  The tensor core truncates fp32 operands to tf32 (probe mode
-// 1), so the raw value IS the hi part; lo = x - trunc(x) is exact in fp32.
-// The A operand stacks the filters as 128 rows, row 2c = W[c] (hi), row 2c+1
-// = W[c] - trunc(W[c]) (lo), and each 16-channel tap issues D += A.Xhi,
-// D += A.Xlo per 8 channels: row 2c accumulates Whi.(Xhi + Xlo), row 2c+1
-// Wlo.(Xhi + Xlo); the epilogue adds the row pair (3xTF32 plus the lo.lo
-// term).  Two N = NT MMAs per 8 channels for 64 output channels x NT pixels.
+// Split TF32 + a bf16 correction.  The tensor core truncates fp32 operands to
+// tf32 (probe mode 1), so the raw value IS the hi part; lo = x - trunc(x) is
+// exact in fp32.  Per 16-channel tap: two kind::tf32 MMAs (K = 8 each) with A
+// = 128 rows, row 2c = W[c] (hi after truncation), row 2c+1 = W[c] - trunc(W[c])
+// (lo), against raw X: row 2c accumulates Whi.Xhi, row 2c+1 Wlo.Xhi; and one
+// kind::f16 MMA (K = 16) with A rows 2c = bf16(W[c]), 2c+1 = 0 against the
+// halo's bf16(lo) planes: row 2c += W.Xlo.  The epilogue adds the row pair.
+// The correction term is ~2^-11 of the product, so bf16's 8-bit mantissa
+// leaves ~2^-19 relative error per product (3xTF32: ~2^-21; both far inside
+// the 1e-4 relative rule).  Three MMAs per tap instead of 3xTF32's four
+// (the 4th, lo.lo, was the price of the 2-row-per-channel stacking): 25 %
+// fewer tensor cycles and shared-memory operand reads, which bound this kernel.
 // The filter stage images come from a small prepass (cp_filter_kernel)
 // launched just before this kernel with programmatic dependent launch: only
 // the filter producer waits for it (griddepcontrol.wait), the raw X boxes and
@@ -65,6 +71,8 @@
 //               part: smem transpose, publish / fixup, coalesced NCHW stores
 #pragma once
 
+#include <cuda_bf16.h>
+
 #include "conv_common.cuh"
 
 namespace lsb {
@@ -72,11 +80,11 @@ namespace tc {
 
 constexpr int CP_HALO = 384;                       // halo rows per buffer
 constexpr int CP_PLANE = CP_HALO * 16;             // bytes per 4-channel plane
-constexpr int CP_HALO_BYTES = 8 * CP_PLANE;        // hi planes 0-3, lo planes 4-7: 48 KiB
+constexpr int CP_HALO_BYTES = 6 * CP_PLANE;        // fp32 planes 0-3, bf16 lo planes 4-5: 36 KiB
 constexpr int CP_RAW_BYTES = 28 * 1024;            // raw X slot: 16 channels x rb rows x wb floats
 constexpr int CP_RAW_SLOTS = 2;
 constexpr int CP_FSLOTS = 3;                       // filter ring slots, each a tap pair
-constexpr int CP_FSTAGE = 4 * 128 * 16;            // 8 KiB per tap: 4 planes x 128 rows x 16 B
+constexpr int CP_FSTAGE = 6 * 128 * 16;            // 12 KiB per tap: 4 fp32 + 2 bf16 planes x 128 rows x 16 B
 constexpr int CP_CONV_WARPS = 4;
 constexpr int CP_EPI_WARPS = 8;
 constexpr int CP_THREADS = 64 + 32 * (CP_CONV_WARPS + CP_EPI_WARPS);   // 448
@@ -124,9 +132,9 @@ __device__ __forceinline__ void cp_stamp2(const ConvPlanarArgs &p, int slot) {
 }
 
 // planar filter stage images: stage (cb, tap) of co tile ct holds, for the 16
-// channels cb*16.., rows 2c = W[ct*64 + c] (the hi part: the tensor core
-// truncates) and 2c+1 = W - trunc(W); channels >= C and filters >= CO are
-// zero.  One thread per element e = ((ct * stages + stage) * 64 + co) * 16 + ch.
+// channels cb*16.., fp32 rows 2c = W[ct*64 + c] (the hi part: the tensor core
+// truncates) and 2c+1 = W - trunc(W), then bf16 rows 2c = bf16(W), 2c+1 = 0;
+// channels >= C and filters >= CO are zero.  One thread per element e = ((ct * stages + stage) * 64 + co) * 16 + ch.
 struct CpFilterArgs {
     const float *w;
     int64_t swt[4];
@@ -155,6 +163,10 @@ __global__ void __launch_bounds__(256) cp_filter_kernel(const CpFilterArgs f) {
     const int plane = ch >> 2, q = ch & 3;
     st[plane * 512 + (2 * co_l) * 4 + q] = v;
     st[plane * 512 + (2 * co_l + 1) * 4 + q] = lo;
+    // bf16 planes (after the 4 fp32 planes): [8-channel plane][128 rows][8]
+    __nv_bfloat16 *sb = reinterpret_cast<__nv_bfloat16 *>(st + 4 * 512);
+    sb[(ch >> 3) * 1024 + (2 * co_l) * 8 + (ch & 7)] = __float2bfloat16_rn(fin ? v : 0.0f);
+    sb[(ch >> 3) * 1024 + (2 * co_l + 1) * 8 + (ch & 7)] = __float2bfloat16_rn(0.0f);
     if (!fin) *f.wflag = f.gen;
 }
 
@@ -282,8 +294,14 @@ struct CpIter {
     }
 };
 
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);   // .x = lo (lower address)
+    return *reinterpret_cast<const uint32_t *>(&v);
+}
+
 // a share of a job's halo conversion: rows first, first + step, ... of the
-// raw slot [c][row][wb] -> planar hi / lo; returns true on a non-finite value
+// raw slot [c][row][wb] -> fp32 planes + bf16 lo planes; returns true on a
+// non-finite value
 __device__ __forceinline__ bool cp_convert(const ConvPlanarArgs &p, const float *raw, float *hb, int F0, int first,
                                            int step) {
     const float inf = __int_as_float(0x7f800000);
@@ -294,6 +312,7 @@ __device__ __forceinline__ bool cp_convert(const ConvPlanarArgs &p, const float 
         const int F = F0 + row;
         const int hp = F / p.Wp, wp = F - hp * p.Wp;
         const float *src = raw + (hp - hp0) * p.wb + wp + p.wsh;
+        uint32_t lo2[8];
 #pragma unroll
         for (int g = 0; g < 4; g++) {
             float4 hv = make_float4(src[(4 * g) * cstride], src[(4 * g + 1) * cstride], src[(4 * g + 2) * cstride],
@@ -308,8 +327,11 @@ __device__ __forceinline__ bool cp_convert(const ConvPlanarArgs &p, const float 
                 l4[q] = fin ? x - __uint_as_float(__float_as_uint(x) & 0xffffe000u) : 0.0f;
             }
             *reinterpret_cast<float4 *>(hb + g * (CP_PLANE / 4) + row * 4) = hv;
-            *reinterpret_cast<float4 *>(hb + (4 + g) * (CP_PLANE / 4) + row * 4) = lv;
+            lo2[2 * g] = pack_bf16x2(lv.x, lv.y);
+            lo2[2 * g + 1] = pack_bf16x2(lv.z, lv.w);
         }
+        *reinterpret_cast<uint4 *>(hb + 4 * (CP_PLANE / 4) + row * 4) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
+        *reinterpret_cast<uint4 *>(hb + 5 * (CP_PLANE / 4) + row * 4) = make_uint4(lo2[4], lo2[5], lo2[6], lo2[7]);
     }
     return bad;
 }
@@ -498,7 +520,7 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
         // ---------------- MMA issuer: the whole warp runs the loop, so the
         // descriptor arithmetic is warp-uniform (uniform registers, no
         // per-MMA broadcasts) and one elected lane issues each tcgen05 op
-        constexpr uint32_t idesc = idesc_tf32(128, NT);
+        constexpr uint32_t idesc = idesc_tf32(128, NT), idesc_lo = idesc_bf16(128, NT);
         constexpr uint64_t kPlane = CP_PLANE >> 4, kAPlane = 2048 >> 4;
         int slot = 0, b = 0, njob = 0;
         uint32_t fph = 0, hph[2] = {0, 0}, cph[2] = {0, 0};
@@ -519,7 +541,7 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
             const uint64_t bdesc0 = desc_planar(smem_u32(smem + b * CP_HALO_BYTES), CP_PLANE);
             int r = j.t0 / p.S, s = j.t0 - r * p.S;
             for (int tap = j.t0; tap < j.t1; tap += 2) {
-                // one filter slot = a tap pair: one barrier wait per 8 MMAs
+                // one filter slot = a tap pair: one barrier wait per 6 MMAs
                 const int n = min(2, j.t1 - tap);
                 mbar_wait_sleep(&f_full[slot], fph);
                 tc_fence_after();
@@ -538,14 +560,12 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
                 if (elect_one()) {
                     if (!(p.dbg & 4)) {
                         umma_tf32(d, a0, b0, idesc, tap == j.t0 ? 0u : 1u);
-                        umma_tf32(d, a0, b0 + 4 * kPlane, idesc, 1u);
                         umma_tf32(d, a0 + 2 * kAPlane, b0 + 2 * kPlane, idesc, 1u);
-                        umma_tf32(d, a0 + 2 * kAPlane, b0 + 6 * kPlane, idesc, 1u);
+                        umma_bf16(d, a0 + 4 * kAPlane, b0 + 4 * kPlane, idesc_lo, 1u);
                         if (n == 2) {
                             umma_tf32(d, a1, b1, idesc, 1u);
-                            umma_tf32(d, a1, b1 + 4 * kPlane, idesc, 1u);
                             umma_tf32(d, a1 + 2 * kAPlane, b1 + 2 * kPlane, idesc, 1u);
-                            umma_tf32(d, a1 + 2 * kAPlane, b1 + 6 * kPlane, idesc, 1u);
+                            umma_bf16(d, a1 + 4 * kAPlane, b1 + 4 * kPlane, idesc_lo, 1u);
                         }
                     }
                     umma_commit(&f_empty[slot]);
