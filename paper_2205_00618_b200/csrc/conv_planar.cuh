@@ -134,7 +134,9 @@ __device__ __forceinline__ void cp_stamp2(const ConvPlanarArgs &p, int slot) {
 // planar filter stage images: stage (cb, tap) of co tile ct holds, for the 16
 // channels cb*16.., fp32 rows 2c = W[ct*64 + c] (the hi part: the tensor core
 // truncates) and 2c+1 = W - trunc(W), then bf16 rows 2c = bf16(W), 2c+1 = 0;
-// channels >= C and filters >= CO are zero.  One thread per element e = ((ct * stages + stage) * 64 + co) * 16 + ch.
+// channels >= C and filters >= CO are zero.  One thread per (stage, 4-channel
+// group, filter) -- e = ((ct * stages + stage) * 4 + g) * 64 + co -- writing
+// 16-B hi / lo rows and an 8-B bf16 row piece.
 struct CpFilterArgs {
     const float *w;
     int64_t swt[4];
@@ -149,25 +151,36 @@ __global__ void __launch_bounds__(256) cp_filter_kernel(const CpFilterArgs f) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= f.total) return;
     const float inf = __int_as_float(0x7f800000);
-    const int ch = e & 15, co_l = (e >> 4) & 63, ts = e >> 10;
+    const int co_l = e & 63, g = (e >> 6) & 3, ts = e >> 8;
     const int stage = ts % f.stages, ct = ts / f.stages;
     const int RS = f.R * f.S;
     const int cb = stage / RS, tap = stage - cb * RS;
     const int r = tap / f.S, s = tap - r * f.S;
-    const int co = ct * 64 + co_l, c = cb * 16 + ch;
-    float v = 0.0f;
-    if (co < f.CO && c < f.C) v = __ldg(f.w + co * f.swt[0] + c * f.swt[1] + r * f.swt[2] + s * f.swt[3]);
-    const bool fin = fabsf(v) < inf;
-    const float lo = fin ? v - __uint_as_float(__float_as_uint(v) & 0xffffe000u) : 0.0f;
+    const int co = ct * 64 + co_l, c0 = cb * 16 + 4 * g;
+    float v[4], lo[4];
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        v[q] = (co < f.CO && c0 + q < f.C)
+                   ? __ldg(f.w + co * f.swt[0] + (c0 + q) * f.swt[1] + r * f.swt[2] + s * f.swt[3])
+                   : 0.0f;
+        const bool fin = fabsf(v[q]) < inf;
+        bad |= !fin;
+        lo[q] = fin ? v[q] - __uint_as_float(__float_as_uint(v[q]) & 0xffffe000u) : 0.0f;
+    }
     float *st = f.img + (int64_t)ts * (CP_FSTAGE / 4);
-    const int plane = ch >> 2, q = ch & 3;
-    st[plane * 512 + (2 * co_l) * 4 + q] = v;
-    st[plane * 512 + (2 * co_l + 1) * 4 + q] = lo;
+    *reinterpret_cast<float4 *>(st + g * 512 + (2 * co_l) * 4) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4 *>(st + g * 512 + (2 * co_l + 1) * 4) = make_float4(lo[0], lo[1], lo[2], lo[3]);
     // bf16 planes (after the 4 fp32 planes): [8-channel plane][128 rows][8]
-    __nv_bfloat16 *sb = reinterpret_cast<__nv_bfloat16 *>(st + 4 * 512);
-    sb[(ch >> 3) * 1024 + (2 * co_l) * 8 + (ch & 7)] = __float2bfloat16_rn(fin ? v : 0.0f);
-    sb[(ch >> 3) * 1024 + (2 * co_l + 1) * 8 + (ch & 7)] = __float2bfloat16_rn(0.0f);
-    if (!fin) *f.wflag = f.gen;
+    __nv_bfloat16 *sb = reinterpret_cast<__nv_bfloat16 *>(st + 4 * 512) + (g >> 1) * 1024 + (g & 1) * 4;
+    // (a non-finite filter value keeps hi = the value for the flag path; its
+    // bf16 copy is 0 -- tiles are recomputed in FP32 when wflag is set)
+    const __nv_bfloat162 b01 = __floats2bfloat162_rn(fabsf(v[0]) < inf ? v[0] : 0.0f, fabsf(v[1]) < inf ? v[1] : 0.0f);
+    const __nv_bfloat162 b23 = __floats2bfloat162_rn(fabsf(v[2]) < inf ? v[2] : 0.0f, fabsf(v[3]) < inf ? v[3] : 0.0f);
+    *reinterpret_cast<uint2 *>(sb + (2 * co_l) * 8) =
+        make_uint2(*reinterpret_cast<const uint32_t *>(&b01), *reinterpret_cast<const uint32_t *>(&b23));
+    *reinterpret_cast<uint2 *>(sb + (2 * co_l + 1) * 8) = make_uint2(0u, 0u);
+    if (bad) *f.wflag = f.gen;
 }
 
 // output position of per-image flat column F (false: a dropped position)
