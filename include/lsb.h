@@ -249,6 +249,10 @@ int lsb_host_is_pinned(const void *p, int *pinned);
  * 256), grid size, persistent units (0 = one tile per CTA), 2-CTA clusters.
  * Diagnostics for tests and tools. */
 int lsb_last_gemm_launch(int *bn, int *ctas, int *units, int *pair);
+/* Kernel of the last lsb_conv2d_nchw on this process: 0 SIMT implicit GEMM,
+ * 1 NHWC-copy tensor-core kernel, 2 planar tensor-core kernel (*nt = its
+ * pixel tile, 0 otherwise).  Diagnostics for tests and tools. */
+int lsb_last_conv_kernel(int *kind, int *nt);
 
 /* ---- kernels ---------------------------------------------------------------- */
 int lsb_semiring_gemm(const lsb_gemm_desc *desc, void *stream);

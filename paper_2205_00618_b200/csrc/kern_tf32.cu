@@ -816,6 +816,11 @@ bool conv_planar_ok(const ConvArgs &c, int64_t n_img) {
     return cp_geom(c, n_img, g);
 }
 
+int conv_planar_nt(const ConvArgs &c, int64_t n_img) {
+    CpGeom g;
+    return cp_geom(c, n_img, g) ? g.nt : 0;
+}
+
 int conv_planar(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen) {
     CpGeom g;
     if (!cp_geom(c, n_img, g)) {

@@ -660,6 +660,14 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     return LSB_OK;
 }
 
+static int g_last_conv_kind = 0, g_last_conv_nt = 0;   // lsb_last_conv_kernel (diagnostics)
+
+int lsb_last_conv_kernel(int *kind, int *nt) {
+    if (kind) *kind = g_last_conv_kind;
+    if (nt) *nt = g_last_conv_nt;
+    return LSB_OK;
+}
+
 int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     if (!d) return fail(LSB_ERR_INVALID, "null desc");
     if (!d->x || !d->w || !d->o) return fail(LSB_ERR_INVALID, "null operand");
@@ -706,6 +714,8 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     case lsb::kAlgoTf32x3Planar: tc_mode = planar_ok ? 5 : nhwc_ok ? 4 : 0; break;
     default: break;
     }
+    g_last_conv_kind = tc_mode == 5 ? 2 : tc_mode == 4 ? 1 : 0;
+    g_last_conv_nt = tc_mode == 5 ? lsb::conv_planar_nt(a, d->N) : 0;
     if (tc_mode) {
         char err[256] = "";
         int aux = 0;

@@ -62,6 +62,7 @@ bool tf32x3_conv_nhwc_ok(const ConvArgs &c, int64_t n_img);
 int tf32x3_conv_nhwc(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err,
                      size_t errlen);
 bool conv_planar_ok(const ConvArgs &c, int64_t n_img);
+int conv_planar_nt(const ConvArgs &c, int64_t n_img);   // its pixel tile (0: not eligible)
 int conv_planar(const ConvArgs &c, int64_t n_img, cudaStream_t s, int *aux_launches, char *err, size_t errlen);
 
 template <int C, int R, bool B, int BM, bool TWO = false>

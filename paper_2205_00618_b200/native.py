@@ -117,6 +117,7 @@ _SIGS = {
     "lsb_stage_wait": ([], ctypes.c_int),
     "lsb_host_is_pinned": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "lsb_last_gemm_launch": ([ctypes.POINTER(ctypes.c_int)] * 4, ctypes.c_int),
+    "lsb_last_conv_kernel": ([ctypes.POINTER(ctypes.c_int)] * 2, ctypes.c_int),
     "lsb_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
     "lsb_nccl_init": ([ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)], ctypes.c_int),
     "lsb_nccl_destroy": ([vp], ctypes.c_int),
@@ -312,6 +313,14 @@ def last_gemm_launch() -> dict:
     v = [ctypes.c_int() for _ in range(4)]
     check(lib().lsb_last_gemm_launch(*(ctypes.byref(x) for x in v)), "lsb_last_gemm_launch")
     return dict(zip(("bn", "ctas", "units", "pair"), (x.value for x in v)))
+
+
+def last_conv_kernel() -> tuple:
+    """(kind, nt) of the last conv launch: kind 0 SIMT, 1 NHWC-copy tensor-core,
+    2 planar tensor-core (nt = its pixel tile)."""
+    k, nt = ctypes.c_int(), ctypes.c_int()
+    check(lib().lsb_last_conv_kernel(ctypes.byref(k), ctypes.byref(nt)), "lsb_last_conv_kernel")
+    return k.value, nt.value
 
 
 def d2d(dst: int, src: int, nbytes: int, stream: int = 0) -> None:
