@@ -574,11 +574,11 @@ __global__ void __launch_bounds__(CP_THREADS, 1)
                     if (!(p.dbg & 4)) {
                         umma_tf32(d, a0, b0, idesc, tap == j.t0 ? 0u : 1u);
                         umma_tf32(d, a0 + 2 * kAPlane, b0 + 2 * kPlane, idesc, 1u);
-                        umma_bf16(d, a0 + 4 * kAPlane, b0 + 4 * kPlane, idesc_lo, 1u);
+                        umma_f16(d, a0 + 4 * kAPlane, b0 + 4 * kPlane, idesc_lo, 1u);
                         if (n == 2) {
                             umma_tf32(d, a1, b1, idesc, 1u);
                             umma_tf32(d, a1 + 2 * kAPlane, b1 + 2 * kPlane, idesc, 1u);
-                            umma_bf16(d, a1 + 4 * kAPlane, b1 + 4 * kPlane, idesc_lo, 1u);
+                            umma_f16(d, a1 + 4 * kAPlane, b1 + 4 * kPlane, idesc_lo, 1u);
                         }
                     }
                     umma_commit(&f_empty[slot]);

@@ -128,24 +128,41 @@ float *acquire_ws(size_t need, char *err, size_t errlen) {
 // split prepass of one operand viewed as X[r][k] = X[r*s_r + k*s_k] -> hi/lo
 // [R][Kp]: the vectorised kernels when the layout allows, else the scalar one
 void launch_split(const float *X, int64_t R, int64_t Kd, int64_t s_r, int64_t s_k, float *hi, float *lo, int64_t Kp,
-                  int ilv, int *flag, int *any, int gen, cudaStream_t s) {
+                  int ilv, int *flag, int *any, int gen, cudaStream_t s, int *gmax = nullptr, int group = 1) {
+    if (ilv) {
+        // the fp16 cross terms' scale source: finite max |x| per row (A) or
+        // per 128-row group of the transposed B (split_exp)
+        cudaMemsetAsync(gmax, 0, sizeof(int) * (size_t)((R + group - 1) / group), s);
+        if (s_k == 1) {
+            const bool vec = reinterpret_cast<uintptr_t>(X) % 16 == 0 && s_r % 4 == 0 && Kd % 4 == 0;
+            tc::split_max_kcontig_kernel<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(X, R, Kd, s_r, group, vec ? 1 : 0,
+                                                                                 gmax);
+        } else {
+            // threads along r; K cut into slices so the grid fills the GPU
+            const int64_t rblocks = (R + 255) / 256;
+            const int64_t kslices = std::max<int64_t>(1, std::min<int64_t>(Kd, (4 * 148 + rblocks - 1) / rblocks));
+            const int64_t kchunk = (Kd + kslices - 1) / kslices;
+            dim3 g((unsigned)rblocks, (unsigned)((Kd + kchunk - 1) / kchunk));
+            tc::split_max_rows_kernel<<<g, 256, 0, s>>>(X, R, Kd, s_r, s_k, group, kchunk, gmax);
+        }
+    }
     const bool small = R * Kp < (1ll << 31) && R * std::max<int64_t>(s_r, 1) + Kd * std::max<int64_t>(s_k, 1) < (1ll << 31);
     const bool al = reinterpret_cast<uintptr_t>(X) % 16 == 0 && Kp % 4 == 0;
     if (small && al && s_k == 1 && s_r % 4 == 0 && Kd % 4 == 0 && !knobs().scalar_split) {
         const int64_t units = R * (Kp / 4);
         const unsigned blocks = (unsigned)std::min<int64_t>((units + 255) / 256, 148 * 16);
         tc::tf32_split_kcontig_kernel<<<blocks, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_r, hi, lo, (int)Kp, ilv, flag,
-                                                              any, gen);
+                                                              any, gen, gmax, group);
         return;
     }
     if (small && al && s_r == 1 && s_k % 4 == 0 && R % 4 == 0 && !knobs().scalar_split) {
         dim3 g((unsigned)((Kp + 31) / 32), (unsigned)((R + 31) / 32));
         tc::tf32_split_rcontig_kernel<<<g, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_k, hi, lo, (int)Kp, ilv, flag, any,
-                                                              gen);
+                                                              gen, gmax, group);
         return;
     }
     dim3 g((unsigned)((Kp + 31) / 32), (unsigned)((R + 31) / 32));
-    tc::tf32_split_kernel<<<g, 256, 0, s>>>(X, R, Kd, s_r, s_k, hi, lo, Kp, ilv, flag, any, gen);
+    tc::tf32_split_kernel<<<g, 256, 0, s>>>(X, R, Kd, s_r, s_k, hi, lo, Kp, ilv, flag, any, gen, gmax, group);
 }
 
 bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int bk, int box_rows) {
@@ -410,11 +427,11 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
         g_bkey = key;
     }
     float *bhi = ws, *blo = bhi + N * Kp, *ahi = blo + N * Kp, *alo = ahi + M * Kp;
-    int *colflag, *rowflag, *anyflag, *done, agen, bgen;
+    int *colflag, *rowflag, *anyflag, *done, *amax, *bmax, agen, bgen;
     {
         std::lock_guard<std::mutex> lk(g_tc_mu);
         bool fresh = false;
-        if (!grow_flags(M + N + 4, s, &fresh)) {
+        if (!grow_flags(2 * M + N + (N + tc::kBScaleCols - 1) / tc::kBScaleCols + 4, s, &fresh)) {
             snprintf(err, errlen, "cudaMalloc of the non-finite flags failed");
             return LSB_ERR_NOMEM;
         }
@@ -427,15 +444,19 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
         done = g_flags + 2;
         colflag = g_flags + 4;
         rowflag = colflag + N;
+        amax = rowflag + M;     // [anyA, anyB, done, pad | colflag[N] | rowflag[M] | amax[M] | bmax[N/128]]
+        bmax = amax + M;
         agen = ++g_gen;
         if (agen <= 0) agen = g_gen = 1;   // (2^31 calls) never 0, the zeroed state
         if (!reuse_b) g_bgen = agen;
         bgen = g_bgen;
     }
     {
-        launch_split(A, M, K, sa_m, sa_k, ahi, alo, Kp, ilv, rowflag, anyflag, agen, s);
-        if (!reuse_b) launch_split(B, N, K, sb_n, sb_k, bhi, blo, Kp, ilv, colflag, anyflag + 1, bgen, s);
-        if (aux_launches) *aux_launches = reuse_b ? 1 : 2;
+        launch_split(A, M, K, sa_m, sa_k, ahi, alo, Kp, ilv, rowflag, anyflag, agen, s, amax, 1);
+        if (!reuse_b)
+            launch_split(B, N, K, sb_n, sb_k, bhi, blo, Kp, 2 * ilv, colflag, anyflag + 1, bgen, s, bmax,
+                         tc::kBScaleCols);
+        if (aux_launches) *aux_launches = (reuse_b ? 1 : 2) * (ilv ? 2 : 1);   // max pass + split per operand
     }
     tc::TcArgs a;
     memset(&a, 0, sizeof(a));
@@ -443,6 +464,8 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
     a.C = C; a.sc_m = sc_m; a.sc_n = sc_n; a.c_vec = c_vec;
     a.epi = epi;
     a.rowflag = rowflag; a.colflag = colflag; a.anyflag = anyflag; a.done = done; a.agen = agen; a.bgen = bgen;
+    a.amax = ilv ? amax : nullptr;
+    a.bmax = ilv ? bmax : nullptr;
     a.ahi = ahi; a.alo = alo; a.bhi = bhi; a.blo = blo;
     a.ilv = ilv;
     set_fast_epilogue(a, epi);
@@ -652,7 +675,7 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
         }
         g_bkey = BKey{};   // a blocked sequence owns the workspace
         ws = g_split;
-        if (!grow_flags(M + N + 4, s, nullptr)) {
+        if (!grow_flags(2 * M + N + (N + tc::kBScaleCols - 1) / tc::kBScaleCols + 4, s, nullptr)) {
             snprintf(err, errlen, "cudaMalloc of the non-finite flags failed");
             return LSB_ERR_NOMEM;
         }
@@ -660,21 +683,26 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
     }
     float *bhi = ws, *blo = bhi + N * Kp, *ahi = blo + N * Kp, *alo = ahi + M * Kp;
     int *anyflag = flags, *done = flags + 2, *colflag = flags + 4, *rowflag = colflag + N;
+    int *amax = rowflag + M, *bmax = amax + M;
     const int64_t rowlen = ilv ? 2 * Kp : Kp;
     int aux = 0;
     if (d->flags & LSB_GEMM_PREP_A) {
         const int64_t r0 = std::max<int64_t>(0, d->m_begin), r1 = d->m_end > 0 ? std::min(d->m_end, M) : M;
         if (r1 > r0)
             launch_split(d->A + r0 * d->sa_m, r1 - r0, K, d->sa_m, d->sa_k, ahi + r0 * rowlen, alo + r0 * Kp, Kp, ilv,
-                         rowflag + r0, anyflag, d->gen, s);
-        aux++;
+                         rowflag + r0, anyflag, d->gen, s, amax + r0, 1);
+        aux += ilv ? 2 : 1;
     }
     if (d->flags & LSB_GEMM_PREP_B) {
         const int64_t c0 = std::max<int64_t>(0, d->n_begin), c1 = d->n_end > 0 ? std::min(d->n_end, N) : N;
+        if (ilv && c0 % tc::kBScaleCols) {
+            snprintf(err, errlen, "PREP_B columns must start on a %d-column scale block", tc::kBScaleCols);
+            return LSB_ERR_INVALID;
+        }
         if (c1 > c0)
-            launch_split(d->B + c0 * d->sb_n, c1 - c0, K, d->sb_n, d->sb_k, bhi + c0 * rowlen, blo + c0 * Kp, Kp, ilv,
-                         colflag + c0, anyflag + 1, d->gen, s);
-        aux++;
+            launch_split(d->B + c0 * d->sb_n, c1 - c0, K, d->sb_n, d->sb_k, bhi + c0 * rowlen, blo + c0 * Kp, Kp,
+                         2 * ilv, colflag + c0, anyflag + 1, d->gen, s, bmax + c0 / tc::kBScaleCols, tc::kBScaleCols);
+        aux += ilv ? 2 : 1;
     }
     if (aux_launches) *aux_launches = aux;
     if (!(d->flags & LSB_GEMM_PRESPLIT)) return LSB_OK;
@@ -698,6 +726,8 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
     a.C = d->C; a.sc_m = d->sc_m; a.sc_n = d->sc_n; a.c_vec = c_vec;
     a.epi = epi;
     a.rowflag = rowflag; a.colflag = colflag; a.anyflag = anyflag; a.done = done; a.agen = d->gen; a.bgen = d->gen;
+    a.amax = ilv ? amax : nullptr;
+    a.bmax = ilv ? bmax : nullptr;
     a.ahi = ahi; a.alo = alo; a.bhi = bhi; a.blo = blo;
     a.ilv = ilv;
     auto rect = [&](int64_t rm0, int64_t rm1, int64_t rn0, int64_t rn1, int &mt, int &nt, int &mts, int &nts) {

@@ -1,11 +1,23 @@
 // tf32x3_gemm.cuh -- fp32-accurate (mul, add) contraction on the 5th-gen
-// tensor cores: split-TF32 ("3xTF32") with tcgen05.mma, TMEM accumulators,
-// TMA + mbarrier pipelines, warp-specialised roles.
+// tensor cores: split TF32 with tcgen05.mma, TMEM accumulators, TMA +
+// mbarrier pipelines, warp-specialised roles.
 //
-//   C = A.B  ~=  Ahi.Bhi + Ahi.Blo + Alo.Bhi        hi = rna_tf32(x), lo = rna_tf32(x - hi)
+//   C = A.B  ~=  Ahi.Bhi + Ahi.Blo + Alo.Bhi        hi = rna_tf32(x), lo = x - hi
 //
-// The dropped Alo.Blo term is ~2^-22 relative; each split keeps ~2^-23, so a
-// product carries ~fp32 error.  Accumulation is two-level: the tensor core
+// Interleaved operand rows (ilv, the default): per 8-deep k step ONE
+// kind::tf32 MMA computes Ahi.Bhi and ONE kind::f16 MMA (K = 16) computes both
+// cross terms over the stacked fp16 operands [Ahi | Alo] . [Blo ; Bhi] -- two
+// MMA slots per k step instead of 3xTF32's three (C5 +24 %).  fp16 carries
+// tf32's 11-bit significand, so hi is exact in fp16 and lo keeps 11 bits, as
+// 3xTF32's tf32 lo does: the same ~2^-22 error per product.  fp16's range is
+// made to fit by power-of-two scaling: each A row and each 128-column block of
+// B is scaled so its largest finite |x| lies in [2^14, 2^15) (the prepass,
+// `split_exp`), and the epilogue multiplies the accumulator back by
+// 2^(e_row + e_block) -- exact.  Values far below their row's / block's
+// maximum lose fp16 bits in their lo part as subnormals: an absolute error
+// below 2^-40 of the row maximum per product, far inside the VM's own fp32
+// error.  The dropped Alo.Blo term is ~2^-24 relative.  Separate hi/lo
+// buffers (ilv = 0, the BK = 32 geometry on request) keep three tf32 MMAs.  Accumulation is two-level: the tensor core
 // accumulates one K chunk (kChunkK) into a TMEM buffer, the epilogue warps
 // fold finished chunks into fp32 registers (round-to-nearest) while the MMA
 // warp fills the other TMEM buffer.  The chunk is short because the tensor
@@ -25,6 +37,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "lsb_common.cuh"
 
@@ -32,7 +45,12 @@ namespace lsb {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int kChunkK = 64;            // K per TMEM accumulation chunk (see header)
+// K per TMEM accumulation chunk (see header).  128: with two MMA slots per
+// k step a 64-K chunk took as long as the epilogue's TMEM read of the
+// 128x256 accumulator (~2k cycles), which then paced the kernel (measured
+// C5: 243 TF at 64, 266 at 128, same box); 128-K chunks keep the strict
+// rule on C4 (K = 1024) and the golden cases.
+constexpr int kChunkK = 128;
 
 // Tile / stage geometry (the launcher picks by shape):
 //   <16, 128>  64-B K rows (SWIZZLE_64B), 3 stages, ~97 KiB: two CTAs per SM,
@@ -113,6 +131,9 @@ struct TcArgs {
     float *split_ws;
     int *split_cnt;
     const int *rowflag, *colflag, *anyflag;   // anyflag[0] A, [1] B
+    // ilv: per-A-row and per-128-column-block-of-B finite maxima (float bits,
+    // the prepass's scale source, split_exp); the epilogue unscales by them
+    const int *amax, *bmax;
     int *done;                                 // CTA completion counter
     int agen, bgen;
     const float *ahi, *alo, *bhi, *blo;
@@ -228,12 +249,17 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
+// instruction descriptor: kind::f16 with fp16 A/B, fp32 accumulate, K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+    return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
 // instruction descriptor: kind::f16 with bf16 A/B, fp32 accumulate, K-major, M x N
 __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                           uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -303,6 +329,97 @@ __device__ __forceinline__ float tf32_lo(float x, float h) {
 
 // ---------------------------------------------------------------- prepass
 
+constexpr int kBScaleCols = 128;   // B columns sharing one scale (an epilogue warp's column half)
+
+// scale exponent of a group from its largest finite |x| (float bits): the
+// group is multiplied by 2^-e so that max lies in [2^14, 2^15), below fp16's
+// 65504 with one binade to spare; 0 for an all-zero (or empty) group
+__device__ __forceinline__ int split_exp(int maxbits) {
+    const float m = __int_as_float(maxbits);
+    return m > 0.0f ? ilogbf(m) - 14 : 0;
+}
+
+// x * 2^e for the unscaling epilogue (e in [-326, 226]: two steps when 2^e
+// itself is not a normal float)
+__device__ __forceinline__ float scale_pow2(float x, int e) {
+    if (e >= -126 && e <= 127) return x * __int_as_float((e + 127) << 23);
+    return ldexpf(x, e);
+}
+
+// interleaved rows (ilv 1: A operand, 2: B operand): per 16-deep k block
+// 128 B = 16 fp32 hi values, then 32 fp16, per 8-k group g: A [fp16(hi) x 8 |
+// fp16(lo) x 8], B [fp16(lo) x 8 | fp16(hi) x 8], so one K = 16 MMA pairs hi
+// with lo and lo with hi.  `row` = the row's first float.
+__device__ __forceinline__ __half *corr_slot(float *row, int64_t k, int ilv, bool lo) {
+    __half *c = reinterpret_cast<__half *>(row + (k >> 4) * 32 + 16);
+    const int g = (int)((k & 15) >> 3), i = (int)(k & 7);
+    return c + g * 16 + ((ilv == 2) != lo ? 8 : 0) + i;
+}
+__device__ __forceinline__ uint2 half4(float a, float b, float c, float d) {
+    const __half2 u = __floats2half2_rn(a, b), v = __floats2half2_rn(c, d);
+    return make_uint2(*reinterpret_cast<const uint32_t *>(&u), *reinterpret_cast<const uint32_t *>(&v));
+}
+// hi / lo of a scaled value: hi = rna_tf32(x), lo = x - hi (exact); a
+// non-finite x keeps hi = x, lo = 0 (its row / column is recomputed in FP32)
+__device__ __forceinline__ float split_lo(float x, float h) {
+    return fabsf(h) == __int_as_float(0x7f800000) || x != x ? 0.0f : x - h;
+}
+
+// largest finite |X[r][k]| per group of `group` consecutive r, as float bits
+// (non-negative floats order like ints) into gmax[r / group] by atomicMax;
+// the host zeroes gmax.  k-contiguous X: one warp per row, float4 loads when
+// aligned; otherwise threads along r (coalesced for r-contiguous X), each
+// over a `kchunk` slice of k.
+__global__ void __launch_bounds__(256) split_max_kcontig_kernel(const float *__restrict__ X, int64_t R, int64_t Kd,
+                                                                int64_t s_r, int group, int vec,
+                                                                int *__restrict__ gmax) {
+    const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= R) return;
+    const float inf = __int_as_float(0x7f800000);
+    const float *row = X + r * s_r;
+    float m = 0.0f;
+    if (vec) {
+        for (int64_t k = (int64_t)lane * 4; k < Kd; k += 128) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(row + k));
+            const float a[4] = {fabsf(v.x), fabsf(v.y), fabsf(v.z), fabsf(v.w)};
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (a[q] < inf) m = fmaxf(m, a[q]);
+        }
+    } else {
+        for (int64_t k = lane; k < Kd; k += 32) {
+            const float a = fabsf(__ldg(row + k));
+            if (a < inf) m = fmaxf(m, a);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0 && m > 0.0f) atomicMax(gmax + r / group, __float_as_int(m));
+}
+
+__global__ void __launch_bounds__(256) split_max_rows_kernel(const float *__restrict__ X, int64_t R, int64_t Kd,
+                                                             int64_t s_r, int64_t s_k, int group, int64_t kchunk,
+                                                             int *__restrict__ gmax) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t k0 = (int64_t)blockIdx.y * kchunk, k1 = min(Kd, k0 + kchunk);
+    const float inf = __int_as_float(0x7f800000);
+    float m = 0.0f;
+    if (r < R)
+        for (int64_t k = k0; k < k1; k++) {
+            const float a = fabsf(__ldg(X + r * s_r + k * s_k));
+            if (a < inf) m = fmaxf(m, a);
+        }
+    // lanes of one group reduce together (groups are multiples of 32 rows, or 1)
+    if (group >= 32) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0 && r < R && m > 0.0f) atomicMax(gmax + r / group, __float_as_int(m));
+    } else if (r < R && m > 0.0f) {
+        atomicMax(gmax + r / group, __float_as_int(m));
+    }
+}
+
 // X element (r, k) = X[r*s_r + k*s_k]  ->  hi/lo[r][k] (row-major, Kp columns,
 // zero padded).  32x32 tiles through smem so both the read (whichever stride
 // is 1) and the write (k fastest) are coalesced.
@@ -310,7 +427,8 @@ __device__ __forceinline__ float tf32_lo(float x, float h) {
 __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict__ X, int64_t R, int64_t Kd,
                                                          int64_t s_r, int64_t s_k, float *__restrict__ hi,
                                                          float *__restrict__ lo, int64_t Kp, int ilv,
-                                                         int *__restrict__ flag, int *__restrict__ any, int gen) {
+                                                         int *__restrict__ flag, int *__restrict__ any, int gen,
+                                                         const int *__restrict__ gmax, int group) {
     __shared__ float tile[32][33];
     const int64_t r0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
@@ -330,10 +448,18 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
         int64_t r = r0 + a, k = k0 + tx;
         if (r < R && k < Kp) {
             float x = tile[a][tx];
-            float h = rna_tf32(x);
-            const int64_t o = ilv ? r * 2 * Kp + (k >> 4) * 32 + (k & 15) : r * Kp + k;
-            hi[o] = h;
-            (ilv ? hi + 16 : lo)[o] = tf32_lo(x, h);
+            if (ilv) {
+                const float xs = ldexpf(x, -split_exp(gmax[r / group]));
+                const float h = rna_tf32(xs), l = split_lo(xs, h);
+                float *row = hi + r * 2 * Kp;
+                row[(k >> 4) * 32 + (k & 15)] = h;
+                *corr_slot(row, k, ilv, false) = __float2half_rn(h);
+                *corr_slot(row, k, ilv, true) = __float2half_rn(l);
+            } else {
+                const float h = rna_tf32(x);
+                hi[r * Kp + k] = h;
+                lo[r * Kp + k] = tf32_lo(x, h);
+            }
             if (flag != nullptr && !(fabsf(x) < __int_as_float(0x7f800000))) {
                 flag[r] = gen;
                 *any = gen;
@@ -355,11 +481,31 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
 __device__ __forceinline__ int64_t split_off(int64_t r, int64_t k, int64_t Kp, int ilv) {
     return ilv ? r * 2 * Kp + (k >> 4) * 32 + (k & 15) : r * Kp + k;
 }
+// 4 consecutive k (k % 4 == 0) of row r: fp32 hi / lo planes (ilv 0), or the
+// scaled hi and its fp16 correction pairs in an interleaved row
+__device__ __forceinline__ void split_store4(float *hi, float *lo, int64_t r, int64_t k, int64_t Kp, int ilv,
+                                             float4 v, int e) {
+    if (ilv) {
+        v = make_float4(ldexpf(v.x, -e), ldexpf(v.y, -e), ldexpf(v.z, -e), ldexpf(v.w, -e));
+        const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+        float *row = hi + r * 2 * Kp;
+        *reinterpret_cast<float4 *>(row + (k >> 4) * 32 + (k & 15)) = h;
+        *reinterpret_cast<uint2 *>(corr_slot(row, k, ilv, false)) = half4(h.x, h.y, h.z, h.w);
+        *reinterpret_cast<uint2 *>(corr_slot(row, k, ilv, true)) =
+            half4(split_lo(v.x, h.x), split_lo(v.y, h.y), split_lo(v.z, h.z), split_lo(v.w, h.w));
+    } else {
+        const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
+        *reinterpret_cast<float4 *>(hi + r * Kp + k) = h;
+        *reinterpret_cast<float4 *>(lo + r * Kp + k) =
+            make_float4(tf32_lo(v.x, h.x), tf32_lo(v.y, h.y), tf32_lo(v.z, h.z), tf32_lo(v.w, h.w));
+    }
+}
 
 __global__ void __launch_bounds__(256) tf32_split_kcontig_kernel(const float *__restrict__ X, int R, int Kd, int s_r,
                                                                  float *__restrict__ hi, float *__restrict__ lo,
                                                                  int Kp, int ilv, int *__restrict__ flag,
-                                                                 int *__restrict__ any, int gen) {
+                                                                 int *__restrict__ any, int gen,
+                                                                 const int *__restrict__ gmax, int group) {
     asm volatile("griddepcontrol.launch_dependents;");
     const int q4 = Kp / 4;
     const int total = R * q4;
@@ -368,11 +514,7 @@ __global__ void __launch_bounds__(256) tf32_split_kcontig_kernel(const float *__
         const int r = e / q4, k = (e - r * q4) * 4;
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (k < Kd) v = __ldg(reinterpret_cast<const float4 *>(X + (int64_t)r * s_r + k));
-        const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
-        const int64_t o = split_off(r, k, Kp, ilv);
-        *reinterpret_cast<float4 *>(hi + o) = h;
-        *reinterpret_cast<float4 *>((ilv ? hi + 16 : lo) + o) =
-            make_float4(tf32_lo(v.x, h.x), tf32_lo(v.y, h.y), tf32_lo(v.z, h.z), tf32_lo(v.w, h.w));
+        split_store4(hi, lo, r, k, Kp, ilv, v, ilv ? split_exp(gmax[r / group]) : 0);
         if (flag != nullptr && !(fabsf(v.x) < inf && fabsf(v.y) < inf && fabsf(v.z) < inf && fabsf(v.w) < inf)) {
             flag[r] = gen;
             *any = gen;
@@ -383,7 +525,8 @@ __global__ void __launch_bounds__(256) tf32_split_kcontig_kernel(const float *__
 __global__ void __launch_bounds__(256) tf32_split_rcontig_kernel(const float *__restrict__ X, int R, int Kd, int s_k,
                                                                  float *__restrict__ hi, float *__restrict__ lo,
                                                                  int Kp, int ilv, int *__restrict__ flag,
-                                                                 int *__restrict__ any, int gen) {
+                                                                 int *__restrict__ any, int gen,
+                                                                 const int *__restrict__ gmax, int group) {
     asm volatile("griddepcontrol.launch_dependents;");
     __shared__ float tile[32][33];   // [k][r]
     const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
@@ -403,11 +546,7 @@ __global__ void __launch_bounds__(256) tf32_split_rcontig_kernel(const float *__
     const int r = r0 + rr, k = k0 + k4;
     if (r < R && k < Kp) {
         const float4 v = make_float4(tile[k4][rr], tile[k4 + 1][rr], tile[k4 + 2][rr], tile[k4 + 3][rr]);
-        const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
-        const int64_t o = split_off(r, k, Kp, ilv);
-        *reinterpret_cast<float4 *>(hi + o) = h;
-        *reinterpret_cast<float4 *>((ilv ? hi + 16 : lo) + o) =
-            make_float4(tf32_lo(v.x, h.x), tf32_lo(v.y, h.y), tf32_lo(v.z, h.z), tf32_lo(v.w, h.w));
+        split_store4(hi, lo, r, k, Kp, ilv, v, ilv ? split_exp(gmax[r / group]) : 0);
         const float inf = __int_as_float(0x7f800000);
         if (flag != nullptr && !(fabsf(v.x) < inf && fabsf(v.y) < inf && fabsf(v.z) < inf && fabsf(v.w) < inf)) {
             flag[r] = gen;
@@ -439,11 +578,16 @@ __device__ void tc_nonfinite_fixup(const TcArgs &p) {
     auto fix = [&](int64_t m, int64_t n) {
         float acc = 0.0f;
         if (p.ilv) {
-            const float *a = p.ahi + m * 2 * p.Kp, *b = p.bhi + n * 2 * p.Kp;
+            // scaled hi + fp16 lo, unscaled at the end: exact for the non-finite
+            // values that flagged this row / column (lo = 0), and every output
+            // here has one
+            float *a = const_cast<float *>(p.ahi) + m * 2 * p.Kp, *b = const_cast<float *>(p.bhi) + n * 2 * p.Kp;
             for (int64_t k = 0; k < p.K; k++) {
                 const int64_t o = (k >> 4) * 32 + (k & 15);
-                acc = fmaf(a[o] + a[o + 16], b[o] + b[o + 16], acc);
+                acc = fmaf(a[o] + __half2float(*corr_slot(a, k, 1, true)), b[o] + __half2float(*corr_slot(b, k, 2, true)),
+                           acc);
             }
+            acc = scale_pow2(acc, split_exp(p.amax[m]) + split_exp(p.bmax[n / kBScaleCols]));
         } else {
             const float *ah = p.ahi + m * p.Kp, *al = p.alo + m * p.Kp, *bh = p.bhi + n * p.Kp,
                         *bl = p.blo + n * p.Kp;
@@ -610,7 +754,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     } else if (warp == 1) {
         // ---------------- MMA issuer (one thread)
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_tf32(BM, BN);
+            constexpr uint32_t idesc = idesc_tf32(BM, BN), idesc_c = idesc_f16(BM, BN);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t gc = 0;   // chunks issued so far (TMEM buffer, phase)
@@ -647,8 +791,13 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                         const uint64_t off = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along K
                         const uint32_t first = (kb == kb_first && k == 0) ? 0u : 1u;
                         umma_tf32(d, ahi + off, bhi + off, idesc, first);
-                        umma_tf32(d, ahi + off, blo + off, idesc, 1u);
-                        umma_tf32(d, alo + off, bhi + off, idesc, 1u);
+                        if (p.ilv) {
+                            // both cross terms: K = 16 fp16 (32 B) in the row's second 64 B
+                            umma_f16(d, alo + off, blo + off, idesc_c, 1u);
+                        } else {
+                            umma_tf32(d, ahi + off, blo + off, idesc, 1u);
+                            umma_tf32(d, alo + off, bhi + off, idesc, 1u);
+                        }
                     }
                     // smem slot free once these MMAs retire; with paired release
                     // one commit per two stages (each commit costs ~45 cycles of
@@ -728,6 +877,15 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                         tot[i4 * 4 + e] = half == 1 ? ov[e] + tot[i4 * 4 + e] : tot[i4 * 4 + e] + ov[e];
                 }
                 if (et == 0) p.split_cnt[stile] = 0;   // re-armed for the next launch
+            }
+        }
+        if (store && p.amax != nullptr && n0 + ch * 128 < p.N) {
+            // undo the prepass's power-of-two scaling of this row and column block
+            const int64_t mr = m0 + row;
+            const int e = (mr < p.M ? split_exp(p.amax[mr]) : 0) + split_exp(p.bmax[(n0 + ch * 128) / kBScaleCols]);
+            if (e != 0) {
+#pragma unroll
+                for (int i = 0; i < 128; i++) tot[i] = scale_pow2(tot[i], e);
             }
         }
         if constexpr (kPersist) {

@@ -9,7 +9,7 @@ O=gpurun_out
 python bench.py --steps 20 --warmup 5 > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > $O/${TAG}_launches.log 2>&1
-for cfg in C5:tf32x3_gemm_kernel C4:tf32x3_gemm_kernel C3:tf32x3_conv_nhwc_kernel C2:maxplus C1:small_gemm; do
+for cfg in C5:tf32x3_gemm_kernel C4:tf32x3_gemm_kernel C3:conv_planar_kernel C2:maxplus C1:small_gemm; do
     c=${cfg%%:*}; k=${cfg#*:}
     timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o $O/${TAG}_ncu_$c \
         python bench.py --config $c --steps 1 --warmup 3 --no-per-config --no-cpu > $O/${TAG}_ncu_$c.log 2>&1
