@@ -127,13 +127,28 @@ float *acquire_ws(size_t need, char *err, size_t errlen) {
 
 // split prepass of one operand viewed as X[r][k] = X[r*s_r + k*s_k] -> hi/lo
 // [R][Kp]: the vectorised kernels when the layout allows, else the scalar one
-void launch_split(const float *X, int64_t R, int64_t Kd, int64_t s_r, int64_t s_k, float *hi, float *lo, int64_t Kp,
-                  int ilv, int *flag, int *any, int gen, cudaStream_t s, int *gmax = nullptr, int group = 1) {
+// (returns the number of kernels launched)
+int launch_split(const float *X, int64_t R, int64_t Kd, int64_t s_r, int64_t s_k, float *hi, float *lo, int64_t Kp,
+                 int ilv, int *flag, int *any, int gen, cudaStream_t s, int *gmax = nullptr, int group = 1) {
+    const bool small = R * Kp < (1ll << 31) && R * std::max<int64_t>(s_r, 1) + Kd * std::max<int64_t>(s_k, 1) < (1ll << 31);
+    const bool al = reinterpret_cast<uintptr_t>(X) % 16 == 0 && Kp % 4 == 0;
+    if (ilv && group == 1 && small && al && s_k == 1 && s_r % 4 == 0 && Kd % 4 == 0 && !knobs().scalar_split) {
+        // per-row scale: max and split in one pass per row (A operand)
+        tc::tf32_split_rows_kernel<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_r, hi, (int)Kp,
+                                                                            ilv, flag, any, gen, gmax);
+        return 1;
+    }
     if (ilv) {
         // the fp16 cross terms' scale source: finite max |x| per row (A) or
         // per 128-row group of the transposed B (split_exp)
         cudaMemsetAsync(gmax, 0, sizeof(int) * (size_t)((R + group - 1) / group), s);
-        if (s_k == 1) {
+        if (s_r == 1 && group % 128 == 0 && small && al && R % 4 == 0 && s_k % 4 == 0) {
+            const int64_t gblocks = (R + 127) / 128;
+            const int64_t kslices = std::max<int64_t>(1, std::min<int64_t>((Kd + 7) / 8, (4 * 148 + gblocks - 1) / gblocks));
+            const int64_t kchunk = (Kd + kslices - 1) / kslices;
+            dim3 g((unsigned)gblocks, (unsigned)((Kd + kchunk - 1) / kchunk));
+            tc::split_max_rcontig_kernel<<<g, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_k, group, (int)kchunk, gmax);
+        } else if (s_k == 1) {
             const bool vec = reinterpret_cast<uintptr_t>(X) % 16 == 0 && s_r % 4 == 0 && Kd % 4 == 0;
             tc::split_max_kcontig_kernel<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(X, R, Kd, s_r, group, vec ? 1 : 0,
                                                                                  gmax);
@@ -146,23 +161,23 @@ void launch_split(const float *X, int64_t R, int64_t Kd, int64_t s_r, int64_t s_
             tc::split_max_rows_kernel<<<g, 256, 0, s>>>(X, R, Kd, s_r, s_k, group, kchunk, gmax);
         }
     }
-    const bool small = R * Kp < (1ll << 31) && R * std::max<int64_t>(s_r, 1) + Kd * std::max<int64_t>(s_k, 1) < (1ll << 31);
-    const bool al = reinterpret_cast<uintptr_t>(X) % 16 == 0 && Kp % 4 == 0;
+    const int n = ilv ? 2 : 1;   // the max pass + the split
     if (small && al && s_k == 1 && s_r % 4 == 0 && Kd % 4 == 0 && !knobs().scalar_split) {
         const int64_t units = R * (Kp / 4);
         const unsigned blocks = (unsigned)std::min<int64_t>((units + 255) / 256, 148 * 16);
         tc::tf32_split_kcontig_kernel<<<blocks, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_r, hi, lo, (int)Kp, ilv, flag,
                                                               any, gen, gmax, group);
-        return;
+        return n;
     }
     if (small && al && s_r == 1 && s_k % 4 == 0 && R % 4 == 0 && !knobs().scalar_split) {
         dim3 g((unsigned)((Kp + 31) / 32), (unsigned)((R + 31) / 32));
         tc::tf32_split_rcontig_kernel<<<g, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_k, hi, lo, (int)Kp, ilv, flag, any,
                                                               gen, gmax, group);
-        return;
+        return n;
     }
     dim3 g((unsigned)((Kp + 31) / 32), (unsigned)((R + 31) / 32));
     tc::tf32_split_kernel<<<g, 256, 0, s>>>(X, R, Kd, s_r, s_k, hi, lo, Kp, ilv, flag, any, gen, gmax, group);
+    return n;
 }
 
 bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int bk, int box_rows) {
@@ -452,11 +467,11 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
         bgen = g_bgen;
     }
     {
-        launch_split(A, M, K, sa_m, sa_k, ahi, alo, Kp, ilv, rowflag, anyflag, agen, s, amax, 1);
+        int n = launch_split(A, M, K, sa_m, sa_k, ahi, alo, Kp, ilv, rowflag, anyflag, agen, s, amax, 1);
         if (!reuse_b)
-            launch_split(B, N, K, sb_n, sb_k, bhi, blo, Kp, 2 * ilv, colflag, anyflag + 1, bgen, s, bmax,
-                         tc::kBScaleCols);
-        if (aux_launches) *aux_launches = (reuse_b ? 1 : 2) * (ilv ? 2 : 1);   // max pass + split per operand
+            n += launch_split(B, N, K, sb_n, sb_k, bhi, blo, Kp, 2 * ilv, colflag, anyflag + 1, bgen, s, bmax,
+                              tc::kBScaleCols);
+        if (aux_launches) *aux_launches = n;
     }
     tc::TcArgs a;
     memset(&a, 0, sizeof(a));
@@ -689,9 +704,8 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
     if (d->flags & LSB_GEMM_PREP_A) {
         const int64_t r0 = std::max<int64_t>(0, d->m_begin), r1 = d->m_end > 0 ? std::min(d->m_end, M) : M;
         if (r1 > r0)
-            launch_split(d->A + r0 * d->sa_m, r1 - r0, K, d->sa_m, d->sa_k, ahi + r0 * rowlen, alo + r0 * Kp, Kp, ilv,
-                         rowflag + r0, anyflag, d->gen, s, amax + r0, 1);
-        aux += ilv ? 2 : 1;
+            aux += launch_split(d->A + r0 * d->sa_m, r1 - r0, K, d->sa_m, d->sa_k, ahi + r0 * rowlen, alo + r0 * Kp,
+                                Kp, ilv, rowflag + r0, anyflag, d->gen, s, amax + r0, 1);
     }
     if (d->flags & LSB_GEMM_PREP_B) {
         const int64_t c0 = std::max<int64_t>(0, d->n_begin), c1 = d->n_end > 0 ? std::min(d->n_end, N) : N;
@@ -700,9 +714,9 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
             return LSB_ERR_INVALID;
         }
         if (c1 > c0)
-            launch_split(d->B + c0 * d->sb_n, c1 - c0, K, d->sb_n, d->sb_k, bhi + c0 * rowlen, blo + c0 * Kp, Kp,
-                         2 * ilv, colflag + c0, anyflag + 1, d->gen, s, bmax + c0 / tc::kBScaleCols, tc::kBScaleCols);
-        aux += ilv ? 2 : 1;
+            aux += launch_split(d->B + c0 * d->sb_n, c1 - c0, K, d->sb_n, d->sb_k, bhi + c0 * rowlen, blo + c0 * Kp,
+                                Kp, 2 * ilv, colflag + c0, anyflag + 1, d->gen, s, bmax + c0 / tc::kBScaleCols,
+                                tc::kBScaleCols);
     }
     if (aux_launches) *aux_launches = aux;
     if (!(d->flags & LSB_GEMM_PRESPLIT)) return LSB_OK;

@@ -50,7 +50,10 @@ constexpr int BM = 128;
 // 128x256 accumulator (~2k cycles), which then paced the kernel (measured
 // C5: 243 TF at 64, 266 at 128, same box); 128-K chunks keep the strict
 // rule on C4 (K = 1024) and the golden cases.
-constexpr int kChunkK = 128;
+#ifndef LSB_CHUNK_K
+#define LSB_CHUNK_K 128   // build-time A/B (tools/dbg): -DLSB_CHUNK_K=64
+#endif
+constexpr int kChunkK = LSB_CHUNK_K;
 
 // Tile / stage geometry (the launcher picks by shape):
 //   <16, 128>  64-B K rows (SWIZZLE_64B), 3 stages, ~97 KiB: two CTAs per SM,
@@ -335,9 +338,21 @@ constexpr int kBScaleCols = 128;   // B columns sharing one scale (an epilogue w
 // group is multiplied by 2^-e so that max lies in [2^14, 2^15), below fp16's
 // 65504 with one binade to spare; 0 for an all-zero (or empty) group
 __device__ __forceinline__ int split_exp(int maxbits) {
-    const float m = __int_as_float(maxbits);
-    return m > 0.0f ? ilogbf(m) - 14 : 0;
+    if (maxbits <= 0) return 0;
+    const int be = (maxbits >> 23) & 0xff;
+    return (be ? be - 127 : ilogbf(__int_as_float(maxbits))) - 14;   // subnormal max: rare
 }
+
+// the prepass scale 2^-e as two normal factors (one when |e| <= 126)
+struct Pow2 {
+    float f1, f2;
+    __device__ __forceinline__ explicit Pow2(int e) {
+        const int e1 = max(-126, min(127, e)), e2 = max(-126, min(127, e - e1));
+        f1 = __int_as_float((e1 + 127) << 23);
+        f2 = __int_as_float((e2 + 127) << 23);
+    }
+    __device__ __forceinline__ float operator()(float x) const { return x * f1 * f2; }
+};
 
 // x * 2^e for the unscaling epilogue (e in [-326, 226]: two steps when 2^e
 // itself is not a normal float)
@@ -449,7 +464,7 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
         if (r < R && k < Kp) {
             float x = tile[a][tx];
             if (ilv) {
-                const float xs = ldexpf(x, -split_exp(gmax[r / group]));
+                const float xs = Pow2(-split_exp(gmax[r / group]))(x);
                 const float h = rna_tf32(xs), l = split_lo(xs, h);
                 float *row = hi + r * 2 * Kp;
                 row[(k >> 4) * 32 + (k & 15)] = h;
@@ -486,7 +501,8 @@ __device__ __forceinline__ int64_t split_off(int64_t r, int64_t k, int64_t Kp, i
 __device__ __forceinline__ void split_store4(float *hi, float *lo, int64_t r, int64_t k, int64_t Kp, int ilv,
                                              float4 v, int e) {
     if (ilv) {
-        v = make_float4(ldexpf(v.x, -e), ldexpf(v.y, -e), ldexpf(v.z, -e), ldexpf(v.w, -e));
+        const Pow2 sc(-e);
+        v = make_float4(sc(v.x), sc(v.y), sc(v.z), sc(v.w));
         const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
         float *row = hi + r * 2 * Kp;
         *reinterpret_cast<float4 *>(row + (k >> 4) * 32 + (k & 15)) = h;
@@ -519,6 +535,78 @@ __global__ void __launch_bounds__(256) tf32_split_kcontig_kernel(const float *__
             flag[r] = gen;
             *any = gen;
         }
+    }
+}
+
+// interleaved split of k-contiguous rows with a per-row scale (the A operand):
+// one warp per row, pass 1 the row's finite max (written to gmax[r], the
+// epilogue's unscale source), pass 2 the split from the same (now cached)
+// row -- no separate max launch, one DRAM read.  Preconditions as the
+// vectorised kcontig kernel.
+__global__ void __launch_bounds__(256) tf32_split_rows_kernel(const float *__restrict__ X, int R, int Kd, int s_r,
+                                                              float *__restrict__ hi, int Kp, int ilv,
+                                                              int *__restrict__ flag, int *__restrict__ any, int gen,
+                                                              int *__restrict__ gmax) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (r >= R) return;
+    const float inf = __int_as_float(0x7f800000);
+    const float *row = X + (int64_t)r * s_r;
+    float m = 0.0f;
+    bool bad = false;
+    for (int k = lane * 4; k < Kd; k += 128) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(row + k));
+        const float a[4] = {fabsf(v.x), fabsf(v.y), fabsf(v.z), fabsf(v.w)};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            if (a[q] < inf) m = fmaxf(m, a[q]);
+            else bad = true;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    bad = __any_sync(0xffffffffu, bad);
+    const int e = split_exp(__float_as_int(m));
+    for (int k = lane * 4; k < Kp; k += 128) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < Kd) v = __ldg(reinterpret_cast<const float4 *>(row + k));
+        split_store4(hi, nullptr, r, k, Kp, ilv, v, e);
+    }
+    if (lane == 0) {
+        gmax[r] = __float_as_int(m);
+        if (bad && flag != nullptr) {
+            flag[r] = gen;
+            *any = gen;
+        }
+    }
+}
+
+// finite max |X[r][k]| per group of `group` (a multiple of 128) consecutive
+// r for r-contiguous X (the [K][N] B operand): a block covers one group
+// (32 lanes x float4 = 128 r) and a slice of k, its 8 warps striding k
+__global__ void __launch_bounds__(256) split_max_rcontig_kernel(const float *__restrict__ X, int R, int Kd, int s_k,
+                                                                int group, int kchunk, int *__restrict__ gmax) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int r = blockIdx.x * 128 + lane * 4;
+    const int k0 = blockIdx.y * kchunk, k1 = min(Kd, k0 + kchunk);
+    const float inf = __int_as_float(0x7f800000);
+    float m = 0.0f;
+    if (r < R)
+        for (int k = k0 + w; k < k1; k += 8) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(X + (int64_t)k * s_k + r));
+            const float a[4] = {fabsf(v.x), fabsf(v.y), fabsf(v.z), fabsf(v.w)};
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (a[q] < inf) m = fmaxf(m, a[q]);
+        }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ float wm[8];
+    if (lane == 0) wm[w] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < 8; i++) m = fmaxf(m, wm[i]);
+        if (m > 0.0f) atomicMax(gmax + (blockIdx.x * 128) / group, __float_as_int(m));
     }
 }
 
@@ -883,10 +971,13 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
             // undo the prepass's power-of-two scaling of this row and column block
             const int64_t mr = m0 + row;
             const int e = (mr < p.M ? split_exp(p.amax[mr]) : 0) + split_exp(p.bmax[(n0 + ch * 128) / kBScaleCols]);
-            if (e != 0) {
+            // two normal power-of-two factors, branch-free per element (a
+            // per-element branch or ldexpf pushed tot[] out of registers:
+            // C4's tile store went from ~15k to ~45k cycles); exact unless
+            // |e| > 126 makes the intermediate subnormal (rows near fp32's limits)
+            const Pow2 sc(e);
 #pragma unroll
-                for (int i = 0; i < 128; i++) tot[i] = scale_pow2(tot[i], e);
-            }
+            for (int i = 0; i < 128; i++) tot[i] = sc(tot[i]);
         }
         if constexpr (kPersist) {
         if (store) {
