@@ -192,11 +192,11 @@ bool make_map(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int 
     return r == CUDA_SUCCESS;
 }
 
-// interleaved split operand: rows of 2*Kp floats ([hi16 | lo16] per k block),
-// box = one k block (32 floats = 128 B) x box_rows, SWIZZLE_128B
+// interleaved fp16 split operand: rows of 2*Kp halves (= Kp float slots;
+// [hi16 | lo16] per 16-k block), box = 128 B (32 k) x box_rows, SWIZZLE_128B
 bool make_map_ilv(CUtensorMap *map, const float *ptr, int64_t rows, int64_t kp, int box_rows) {
-    cuuint64_t dims[2] = {(cuuint64_t)(2 * kp), (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)(2 * kp) * sizeof(float)};
+    cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)kp * sizeof(float)};
     cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(ptr), dims, strides, box,
@@ -699,7 +699,7 @@ int tf32x3_gemm_blocked(const lsb_gemm_desc *d, const EpiStages &epi, int c_vec,
     float *bhi = ws, *blo = bhi + N * Kp, *ahi = blo + N * Kp, *alo = ahi + M * Kp;
     int *anyflag = flags, *done = flags + 2, *colflag = flags + 4, *rowflag = colflag + N;
     int *amax = rowflag + M, *bmax = amax + M;
-    const int64_t rowlen = ilv ? 2 * Kp : Kp;
+    const int64_t rowlen = Kp;   // float slots per split row (fp16 ilv rows: 2 Kp halves)
     int aux = 0;
     if (d->flags & LSB_GEMM_PREP_A) {
         const int64_t r0 = std::max<int64_t>(0, d->m_begin), r1 = d->m_end > 0 ? std::min(d->m_end, M) : M;

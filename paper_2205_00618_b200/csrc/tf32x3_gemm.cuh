@@ -4,20 +4,23 @@
 //
 //   C = A.B  ~=  Ahi.Bhi + Ahi.Blo + Alo.Bhi        hi = rna_tf32(x), lo = x - hi
 //
-// Interleaved operand rows (ilv, the default): per 8-deep k step ONE
-// kind::tf32 MMA computes Ahi.Bhi and ONE kind::f16 MMA (K = 16) computes both
-// cross terms over the stacked fp16 operands [Ahi | Alo] . [Blo ; Bhi] -- two
-// MMA slots per k step instead of 3xTF32's three (C5 +24 %).  fp16 carries
-// tf32's 11-bit significand, so hi is exact in fp16 and lo keeps 11 bits, as
-// 3xTF32's tf32 lo does: the same ~2^-22 error per product.  fp16's range is
-// made to fit by power-of-two scaling: each A row and each 128-column block of
-// B is scaled so its largest finite |x| lies in [2^14, 2^15) (the prepass,
-// `split_exp`), and the epilogue multiplies the accumulator back by
-// 2^(e_row + e_block) -- exact.  Values far below their row's / block's
-// maximum lose fp16 bits in their lo part as subnormals: an absolute error
-// below 2^-40 of the row maximum per product, far inside the VM's own fp32
-// error.  The dropped Alo.Blo term is ~2^-24 relative.  Separate hi/lo
-// buffers (ilv = 0, the BK = 32 geometry on request) keep three tf32 MMAs.  Accumulation is two-level: the tensor core
+// Interleaved fp16 operand rows (ilv, the default): x = hi + lo with
+// hi = fp16(x), lo = fp16(x - hi) -- fp16 carries tf32's 11-bit significand,
+// so the split keeps ~22 bits exactly like 3xTF32's two tf32 parts, and every
+// fp16 x fp16 product is exact in the fp32 accumulator.  Per 16-deep k block
+// three kind::f16 MMAs (K = 16): hi.hi, hi.lo, lo.hi -- 3xTF32's three
+// products at twice the tf32 rate, from half the operand bytes (4 B per
+// element: a 128-B smem row carries 32 k).  fp16's range is made to fit by
+// power-of-two scaling: each A row and each 128-column block of B is scaled so
+// its largest finite |x| lies in [2^14, 2^15) (the prepass, `split_exp`), and
+// the epilogue multiplies the accumulator back by 2^(e_row + e_block) --
+// exact.  Values far below their row's / block's maximum lose low bits as
+// fp16 subnormals: an absolute error below 2^-38 of the row maximum per
+// product, far inside the VM's own fp32 error.  The dropped lo.lo term is
+// ~2^-22 relative, as in 3xTF32.  (Measured path to here: 3xTF32 215 TF on C5;
+// tf32 hi.hi + one fp16 K=16 MMA for both cross terms 260 TF; all-fp16 below.)
+// Separate hi/lo buffers (ilv = 0, the BK = 32 geometry on request) keep the
+// three tf32 MMAs of 3xTF32.  Accumulation is two-level: the tensor core
 // accumulates one K chunk (kChunkK) into a TMEM buffer, the epilogue warps
 // fold finished chunks into fp32 registers (round-to-nearest) while the MMA
 // warp fills the other TMEM buffer.  The chunk is short because the tensor
@@ -361,18 +364,21 @@ __device__ __forceinline__ float scale_pow2(float x, int e) {
     return ldexpf(x, e);
 }
 
-// interleaved rows (ilv 1: A operand, 2: B operand): per 16-deep k block
-// 128 B = 16 fp32 hi values, then 32 fp16, per 8-k group g: A [fp16(hi) x 8 |
-// fp16(lo) x 8], B [fp16(lo) x 8 | fp16(hi) x 8], so one K = 16 MMA pairs hi
-// with lo and lo with hi.  `row` = the row's first float.
-__device__ __forceinline__ __half *corr_slot(float *row, int64_t k, int ilv, bool lo) {
-    __half *c = reinterpret_cast<__half *>(row + (k >> 4) * 32 + 16);
-    const int g = (int)((k & 15) >> 3), i = (int)(k & 7);
-    return c + g * 16 + ((ilv == 2) != lo ? 8 : 0) + i;
-}
+// interleaved fp16 rows (ilv): row r holds Kp "float" slots = 2 Kp halves;
+// per 16-deep k block b: halves [32 b, 32 b + 16) = hi, [32 b + 16, 32 b + 32)
+// = lo (so a 128-B smem row = two k blocks).  `row` = the row's first half.
+__device__ __forceinline__ __half *h16_hi(__half *row, int64_t k) { return row + (k >> 4) * 32 + (k & 15); }
+__device__ __forceinline__ __half *h16_lo(__half *row, int64_t k) { return row + (k >> 4) * 32 + 16 + (k & 15); }
 __device__ __forceinline__ uint2 half4(float a, float b, float c, float d) {
     const __half2 u = __floats2half2_rn(a, b), v = __floats2half2_rn(c, d);
     return make_uint2(*reinterpret_cast<const uint32_t *>(&u), *reinterpret_cast<const uint32_t *>(&v));
+}
+// fp16 split of a scaled value: hi = fp16(x), lo = fp16(x - hi) (x - hi is
+// exact in fp32); a non-finite x keeps hi = x, lo = 0 (its row / column is
+// recomputed in FP32)
+__device__ __forceinline__ void h16_split(float x, float &h, float &l) {
+    h = __half2float(__float2half_rn(x));
+    l = (fabsf(x) < __int_as_float(0x7f800000)) ? x - h : 0.0f;
 }
 // hi / lo of a scaled value: hi = rna_tf32(x), lo = x - hi (exact); a
 // non-finite x keeps hi = x, lo = 0 (its row / column is recomputed in FP32)
@@ -464,12 +470,11 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
         if (r < R && k < Kp) {
             float x = tile[a][tx];
             if (ilv) {
-                const float xs = Pow2(-split_exp(gmax[r / group]))(x);
-                const float h = rna_tf32(xs), l = split_lo(xs, h);
-                float *row = hi + r * 2 * Kp;
-                row[(k >> 4) * 32 + (k & 15)] = h;
-                *corr_slot(row, k, ilv, false) = __float2half_rn(h);
-                *corr_slot(row, k, ilv, true) = __float2half_rn(l);
+                float h, l;
+                h16_split(Pow2(-split_exp(gmax[r / group]))(x), h, l);
+                __half *row = reinterpret_cast<__half *>(hi + r * Kp);
+                *h16_hi(row, k) = __float2half_rn(h);
+                *h16_lo(row, k) = __float2half_rn(l);
             } else {
                 const float h = rna_tf32(x);
                 hi[r * Kp + k] = h;
@@ -493,22 +498,20 @@ __global__ void __launch_bounds__(256) tf32_split_kernel(const float *__restrict
 // Preconditions (checked by the host): 16-B aligned X, the contiguous extent
 // and the other stride multiples of 4, every index < 2^31.
 // (ilv: hi/lo land interleaved in `hi` per 16-k block, see TcArgs::ilv)
-__device__ __forceinline__ int64_t split_off(int64_t r, int64_t k, int64_t Kp, int ilv) {
-    return ilv ? r * 2 * Kp + (k >> 4) * 32 + (k & 15) : r * Kp + k;
-}
 // 4 consecutive k (k % 4 == 0) of row r: fp32 hi / lo planes (ilv 0), or the
 // scaled hi and its fp16 correction pairs in an interleaved row
 __device__ __forceinline__ void split_store4(float *hi, float *lo, int64_t r, int64_t k, int64_t Kp, int ilv,
                                              float4 v, int e) {
     if (ilv) {
         const Pow2 sc(-e);
-        v = make_float4(sc(v.x), sc(v.y), sc(v.z), sc(v.w));
-        const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
-        float *row = hi + r * 2 * Kp;
-        *reinterpret_cast<float4 *>(row + (k >> 4) * 32 + (k & 15)) = h;
-        *reinterpret_cast<uint2 *>(corr_slot(row, k, ilv, false)) = half4(h.x, h.y, h.z, h.w);
-        *reinterpret_cast<uint2 *>(corr_slot(row, k, ilv, true)) =
-            half4(split_lo(v.x, h.x), split_lo(v.y, h.y), split_lo(v.z, h.z), split_lo(v.w, h.w));
+        float h[4], l[4];
+        h16_split(sc(v.x), h[0], l[0]);
+        h16_split(sc(v.y), h[1], l[1]);
+        h16_split(sc(v.z), h[2], l[2]);
+        h16_split(sc(v.w), h[3], l[3]);
+        __half *row = reinterpret_cast<__half *>(hi + r * Kp);
+        *reinterpret_cast<uint2 *>(h16_hi(row, k)) = half4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint2 *>(h16_lo(row, k)) = half4(l[0], l[1], l[2], l[3]);
     } else {
         const float4 h = make_float4(rna_tf32(v.x), rna_tf32(v.y), rna_tf32(v.z), rna_tf32(v.w));
         *reinterpret_cast<float4 *>(hi + r * Kp + k) = h;
@@ -666,15 +669,13 @@ __device__ void tc_nonfinite_fixup(const TcArgs &p) {
     auto fix = [&](int64_t m, int64_t n) {
         float acc = 0.0f;
         if (p.ilv) {
-            // scaled hi + fp16 lo, unscaled at the end: exact for the non-finite
-            // values that flagged this row / column (lo = 0), and every output
-            // here has one
-            float *a = const_cast<float *>(p.ahi) + m * 2 * p.Kp, *b = const_cast<float *>(p.bhi) + n * 2 * p.Kp;
-            for (int64_t k = 0; k < p.K; k++) {
-                const int64_t o = (k >> 4) * 32 + (k & 15);
-                acc = fmaf(a[o] + __half2float(*corr_slot(a, k, 1, true)), b[o] + __half2float(*corr_slot(b, k, 2, true)),
-                           acc);
-            }
+            // scaled fp16 hi + lo, unscaled at the end: exact for the non-finite
+            // values that flagged this row / column (hi = x, lo = 0)
+            __half *a = reinterpret_cast<__half *>(const_cast<float *>(p.ahi) + m * p.Kp);
+            __half *b = reinterpret_cast<__half *>(const_cast<float *>(p.bhi) + n * p.Kp);
+            for (int64_t k = 0; k < p.K; k++)
+                acc = fmaf(__half2float(*h16_hi(a, k)) + __half2float(*h16_lo(a, k)),
+                           __half2float(*h16_hi(b, k)) + __half2float(*h16_lo(b, k)), acc);
             acc = scale_pow2(acc, split_exp(p.amax[m]) + split_exp(p.bmax[n / kBScaleCols]));
         } else {
             const float *ah = p.ahi + m * p.Kp, *al = p.alo + m * p.Kp, *bh = p.bhi + n * p.Kp,
@@ -714,7 +715,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                        const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                        const TcArgs p) {
     using Cf = Cfg<BK_, BN_>;
-    constexpr int BK = Cf::BK, BN = Cf::BN, STAGES = Cf::STAGES, kChunkStages = Cf::kChunkStages;
+    constexpr int BK = Cf::BK, BN = Cf::BN, STAGES = Cf::STAGES;
     constexpr int kTileA = Cf::kTileA, kTileB = Cf::kTileB, kStageBytes = Cf::kStageBytes;
     constexpr int kEpiWarps = Cf::kEpiWarps;
     constexpr bool kPairRelease = (STAGES % 2) == 0;
@@ -730,8 +731,11 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int num_kb = (int)(p.Kp / BK);
-    const int all_chunks = (num_kb + kChunkStages - 1) / kChunkStages;
+    // an interleaved fp16 stage row (128 B) carries 32 k, a fp32 one BK
+    const int kstage = p.ilv ? 2 * BK : BK;
+    const int chunk_stages = kChunkK / kstage;
+    const int num_kb = (int)(p.Kp / kstage);
+    const int all_chunks = (num_kb + chunk_stages - 1) / chunk_stages;
     // unit t -> output tile, K half (-1: whole K) and split-tile slot.
     // grouped raster: consecutive units walk kGroupM m-tiles before moving to
     // the next n-tile, so the CTAs resident together share A and B blocks
@@ -811,14 +815,14 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
             for (int t = blockIdx.x; t < units; t += ustride) {
             const Unit u = decode(t);
             const int64_t m0 = u.m0, n0 = u.n0;
-            const int kb_end = min(num_kb, (u.c_begin + u.num_chunks) * kChunkStages);
-            for (int kb = u.c_begin * kChunkStages; kb < kb_end; kb++) {
+            const int kb_end = min(num_kb, (u.c_begin + u.num_chunks) * chunk_stages);
+            for (int kb = u.c_begin * chunk_stages; kb < kb_end; kb++) {
                 // paired release (even STAGES): a slot pair is freed by one
                 // commit after its second stage (see the MMA loop)
                 mbar_wait(&empty[kPairRelease ? (stage | 1) : stage], phase ^ 1);
                 unsigned char *base = smem + stage * kStageBytes;
                 mbar_expect_tx(&full[stage], kStageBytes);
-                const int kx = kb * BK;
+                const int kx = kb * BK;   // (ilv rows: element 2 kx = byte 128 kb of the row)
                 if (p.ilv && p.pair) {   // own A; half of B (rows crank*BN/2..) into both CTAs
                     tma_load_2d(&map_ahi, &full[stage], base, 2 * kx, (int)m0);
                     tma_load_2d_mc(&map_bhi, &full[stage], base + 2 * kTileA + crank * kTileB, 2 * kx,
@@ -854,35 +858,36 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                 mbar_wait(&tempty[b], tphase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(b * BN);
-                const int kb_first = (u.c_begin + c) * kChunkStages;
-                const int kb_end = min(num_kb, kb_first + kChunkStages);
+                const int kb_first = (u.c_begin + c) * chunk_stages;
+                const int kb_end = min(num_kb, kb_first + chunk_stages);
                 TC_TRACE(2, c);
                 for (int kb = kb_first; kb < kb_end; kb++) {
                     mbar_wait(&full[stage], phase);
                     TC_TRACE(0, kb);
                     tc_fence_after();
                     const uint32_t base = smem_u32(smem + stage * kStageBytes);
-                    uint64_t ahi, alo, bhi, blo;
-                    if (p.ilv) {   // lo = the second 64 B of each 128-B row
-                        ahi = sdesc_k_sw<128>(base);
-                        alo = ahi + (uint64_t)(64 >> 4);
-                        bhi = sdesc_k_sw<128>(base + 2 * kTileA);
-                        blo = bhi + (uint64_t)(64 >> 4);
-                    } else {
-                        ahi = sdesc_k_sw<Cf::kSwizzleBytes>(base);
-                        alo = sdesc_k_sw<Cf::kSwizzleBytes>(base + kTileA);
-                        bhi = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileA);
-                        blo = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileA + kTileB);
-                    }
+                    if (p.ilv) {
+                        // fp16 rows: per 16-k block j bytes [64 j, +32) hi,
+                        // [64 j + 32, +32) lo; three K = 16 MMAs per block
+                        const uint64_t a0 = sdesc_k_sw<128>(base), b0 = sdesc_k_sw<128>(base + 2 * kTileA);
 #pragma unroll
-                    for (int k = 0; k < BK / 8; k++) {
-                        const uint64_t off = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along K
-                        const uint32_t first = (kb == kb_first && k == 0) ? 0u : 1u;
-                        umma_tf32(d, ahi + off, bhi + off, idesc, first);
-                        if (p.ilv) {
-                            // both cross terms: K = 16 fp16 (32 B) in the row's second 64 B
-                            umma_f16(d, alo + off, blo + off, idesc_c, 1u);
-                        } else {
+                        for (int j = 0; j < 2; j++) {
+                            const uint64_t oh = (uint64_t)((64 * j) >> 4), ol = (uint64_t)((64 * j + 32) >> 4);
+                            const uint32_t first = (kb == kb_first && j == 0) ? 0u : 1u;
+                            umma_f16(d, a0 + oh, b0 + oh, idesc_c, first);   // hi.hi
+                            umma_f16(d, a0 + oh, b0 + ol, idesc_c, 1u);      // hi.lo
+                            umma_f16(d, a0 + ol, b0 + oh, idesc_c, 1u);      // lo.hi
+                        }
+                    } else {
+                        const uint64_t ahi = sdesc_k_sw<Cf::kSwizzleBytes>(base);
+                        const uint64_t alo = sdesc_k_sw<Cf::kSwizzleBytes>(base + kTileA);
+                        const uint64_t bhi = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileA);
+                        const uint64_t blo = sdesc_k_sw<Cf::kSwizzleBytes>(base + 2 * kTileA + kTileB);
+#pragma unroll
+                        for (int k = 0; k < BK / 8; k++) {
+                            const uint64_t off = (uint64_t)((k * 32) >> 4);   // 8 tf32 = 32 B along K
+                            const uint32_t first = (kb == kb_first && k == 0) ? 0u : 1u;
+                            umma_tf32(d, ahi + off, bhi + off, idesc, first);
                             umma_tf32(d, ahi + off, blo + off, idesc, 1u);
                             umma_tf32(d, alo + off, bhi + off, idesc, 1u);
                         }
