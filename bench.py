@@ -22,10 +22,10 @@ e2e        the same contraction through the public drop-in API
            ``e2e.pageable`` repeats it from ordinary numpy arrays.
 roofline   dominant kernel's achieved TFLOP/s (algorithmic 2*M*N*K / its own
            average launch duration, CUDA events placed by liblsb around that
-           launch).  Tensor-core GEMM (split TF32 with fp16 cross terms): per
-           8-deep k step one tf32 MMA + one K=16 fp16 MMA, i.e. two bf16-rate
-           MMA slots per 8 fp32 MACs, so the ceiling = measured bf16 dense
-           BURST rate (MEASURED_PEAKS.json) / 4; also against the measured
+           launch).  Tensor-core GEMM (fp16 hi/lo split of scaled operands):
+           per 16-deep k block three K=16 fp16 MMAs (hi.hi, hi.lo, lo.hi), so
+           the ceiling = measured bf16 dense BURST rate (MEASURED_PEAKS.json)
+           / 3; also against the measured
            per-MHz bf16 rate (sustained run / its median clock) x the SM
            clock observed during the timed loop, and (for continuity with
            round 1) against the 3xTF32 ceiling bf16 / 6; SIMT path: the FP32
@@ -548,8 +548,7 @@ def traffic_of(name: str, steps) -> float | None:
 def _frac_clock(achieved, pk, obs, div):
     """achieved / the measured bf16 dense rate per MHz (MEASURED_PEAKS: the
     sustained run and its median SM clock under load) x the SM clock seen
-    during this timed loop, / div (4 = two bf16-rate MMA slots per 8 fp32
-    MACs: one tf32 K=8 + one fp16 K=16)."""
+    during this timed loop, / div (3 = three fp16 MMAs per fp32 MAC)."""
     rate = pk.get("bf16_tflops_sustained")
     clk = (pk.get("clocks_under_load") or {}).get("sm_mhz_median")
     if not (rate and clk and obs):
@@ -560,10 +559,10 @@ def _frac_clock(achieved, pk, obs, div):
 def roofline(steps, achieved, fp32_peak, sm_max, info, clocks, pk, name: str = "") -> dict:
     """Roofline of the dominant kernel (the contraction launch).
 
-    Tensor-core GEMM: per 8-deep k step one kind::tf32 MMA (K = 8) and one
-    kind::f16 MMA (K = 16), each as long as a bf16 K = 16 MMA, so the ceiling
-    for the algorithmic fp32 flops is the measured bf16 dense BURST rate / 4
-    (MEASURED_PEAKS.json, taken near sm_max_mhz); ``frac`` is against it,
+    Tensor-core GEMM: the fp16 hi/lo split runs three kind::f16 MMAs (hi.hi,
+    hi.lo, lo.hi) per fp32 product, so the ceiling for the algorithmic fp32
+    flops is the measured bf16 dense BURST rate / 3 (MEASURED_PEAKS.json,
+    taken near sm_max_mhz); ``frac`` is against it,
     ``frac_at_observed_clock`` against the measured per-MHz rate at the median
     SM clock seen during the timed loop, ``frac_3xtf32_ceiling`` against the
     round-1 algorithm's bf16 / 6.  SIMT path: FP32 peak."""
@@ -571,16 +570,16 @@ def roofline(steps, achieved, fp32_peak, sm_max, info, clocks, pk, name: str = "
                  "(MEASURED_PEAKS sm_max_mhz; no measured FP32 SIMT figure exists)")
     obs = clocks.get("sm_mhz")
     if any("tf32x3" in s for s in steps) and pk.get("bf16_tflops"):
-        peak = pk["bf16_tflops"] / 4.0
+        peak = pk["bf16_tflops"] / 3.0
         out = {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 2),
                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
-               "peak_source": ("measured bf16 dense burst (MEASURED_PEAKS bf16_tflops) / 4: per 8 fp32 MACs "
-                               "one tf32 K=8 MMA + one fp16 K=16 MMA, each a bf16 K=16 MMA's time"),
-               "frac_at_observed_clock": _frac_clock(achieved, pk, obs, 4.0),
-               "peak_sustained": round(pk.get("bf16_tflops_sustained", 0) / 4.0, 2),
+               "peak_source": ("measured bf16 dense burst (MEASURED_PEAKS bf16_tflops) / 3: three fp16 "
+                               "K=16 MMAs (hi.hi, hi.lo, lo.hi) per fp32 product"),
+               "frac_at_observed_clock": _frac_clock(achieved, pk, obs, 3.0),
+               "peak_sustained": round(pk.get("bf16_tflops_sustained", 0) / 3.0, 2),
                "frac_3xtf32_ceiling": round(achieved / (pk["bf16_tflops"] / 6.0), 4),
                "fp32_simt_peak": round(fp32_peak, 2), "x_fp32_simt_peak": round(achieved / fp32_peak, 3),
-               "kernel": "tf32x3_gemm_kernel (tcgen05.mma kind::tf32 + kind::f16, TMEM, TMA)"}
+               "kernel": "tf32x3_gemm_kernel (tcgen05.mma kind::f16 x3 split, TMEM, TMA)"}
         return out
     return {"bound": "fp32", "achieved": round(achieved, 2), "peak": round(fp32_peak, 2),
             "unit": "TFLOP/s", "frac": round(achieved / fp32_peak, 4), "traffic": None,
@@ -710,11 +709,11 @@ def run_gpu(args):
                     per_config[other]["frac_maxplus_ceiling"] = round(g / 1e3 / ceil, 4)
                     per_config[other]["kernel_frac_maxplus_ceiling"] = round(kt / ceil, 4)
                 if pk.get("bf16_tflops") and (any("tf32x3" in s for s in r["steps"]) or other == "C3"):
-                    # the GEMM's algorithm ceiling is bf16 / 4 (see roofline());
+                    # the GEMM's algorithm ceiling is bf16 / 3 (see roofline());
                     # the conv keeps the 3xTF32 ceiling bf16 / 6 as its yardstick
                     # (its MMA mix: two tf32 + one fp16-class MMA per 16 channels
                     # of 64 filters on 128 rows, rows half wasted by the stacking)
-                    ceil = pk["bf16_tflops"] / (6.0 if other == "C3" else 4.0)
+                    ceil = pk["bf16_tflops"] / (6.0 if other == "C3" else 3.0)
                     per_config[other]["tensor_ceiling_tflops"] = round(ceil, 2)
                     per_config[other]["frac_tensor_ceiling"] = round(g / 1e3 / ceil, 4)
                     per_config[other]["kernel_frac_tensor_ceiling"] = round(kt / ceil, 4)
