@@ -26,7 +26,7 @@
  *     (program.py:182-183) so plans carry them verbatim.
  *   - thread-compatible, not thread-safe per stream (like the reference's
  *     CompiledKernel).
- *   - library workspaces (split-K partials, the 3xTF32 split copies, the
+ *   - library workspaces (split-K partials, the tensor-core split copies, the
  *     max-plus fixup slots and flags) are per process and stream-ordered:
  *     contractions enqueued on two different streams at once must not both
  *     need them (run them on one stream, or synchronise in between).
@@ -48,6 +48,10 @@ enum { LSB_OP_ADD = 0, LSB_OP_MUL = 1, LSB_OP_MAX = 2, LSB_OP_MIN = 3 };
 /* elementwise pre/post: program.py:183 EW_CODE (ir.py:179 ELEMENTWISE_OPS) */
 enum { LSB_EW_IDENTITY = 0, LSB_EW_RELU = 1, LSB_EW_SIGMOID = 2 };
 /* GEMM algorithm selector */
+/* LSB_ALGO_TF32X3 names the fp32-accurate tensor-core path (the name is kept
+ * for ABI stability): GEMMs split power-of-two-scaled operands into fp16 hi/lo
+ * parts and run three fp16 tcgen05 MMAs per product (hi.hi, hi.lo, lo.hi),
+ * convs a tf32 + bf16-correction mix; within 1e-5 + 1e-4|ref| per element. */
 enum { LSB_ALGO_AUTO = 0, LSB_ALGO_SIMT = 1, LSB_ALGO_TF32X3 = 2 };
 
 enum {
@@ -245,7 +249,7 @@ int lsb_stage_d2h_2d(void *dst, size_t dpitch, const void *src, size_t spitch,
 int lsb_stage_wait(void);
 /* *pinned = 1 when `p` is page-locked (cudaHostAlloc'd or registered). */
 int lsb_host_is_pinned(const void *p, int *pinned);
-/* Geometry of the last 3xTF32 GEMM launch on this process: tile width (128 /
+/* Geometry of the last tensor-core GEMM launch on this process: tile width (128 /
  * 256), grid size, persistent units (0 = one tile per CTA), 2-CTA clusters.
  * Diagnostics for tests and tools. */
 int lsb_last_gemm_launch(int *bn, int *ctas, int *units, int *pair);
@@ -257,7 +261,8 @@ int lsb_last_conv_kernel(int *kind, int *nt);
 /* ---- kernels ---------------------------------------------------------------- */
 int lsb_semiring_gemm(const lsb_gemm_desc *desc, void *stream);
 /* the LSB_ALGO_* lsb_semiring_gemm will use for `desc` (AUTO resolved:
- * 3xTF32 tensor cores for large batch-1 (mul, add) contractions, else the
+ * the split-precision tensor-core path for large batch-1 (mul, add)
+ * contractions, else the
  * SIMT semiring kernel); < 0 if an explicit request cannot be honoured */
 int lsb_gemm_algo(const lsb_gemm_desc *desc);
 int lsb_conv2d_nchw(const lsb_conv_desc *desc, void *stream);
