@@ -452,7 +452,9 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
             d->beta != 1.0f || d->K == 0)
             return fail(LSB_ERR_UNSUPPORTED, "blocked tf32x3 steps cover batch-1 (mul, add) contractions");
         lsb::EpiStages epi = pack_epi(d->n_epi, d->epi);
-        const int c_vec = (d->sc_n == 1 && aligned16(d->C) && d->sc_m % 4 == 0) ? 1 : 0;
+        const int c_vec = (d->sc_n == 1 && aligned16(d->C) && d->sc_m % 4 == 0)
+                              ? ((reinterpret_cast<uintptr_t>(d->C) % 32 == 0 && d->sc_m % 8 == 0) ? 2 : 1)
+                              : 0;
         char err[256] = "";
         int aux = 0;
         rc = lsb::tf32x3_gemm_blocked(d, epi, c_vec, s, &aux, err, sizeof(err));
@@ -486,6 +488,9 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
     a.a_mode = pick_mode_a(&dd, d->sa_m, d->sa_k);
     a.b_mode = pick_mode_b(&dd);
     a.c_vec = (d->sc_n == 1 && aligned16(a.C) && d->sc_m % 4 == 0 && (d->batch == 1 || d->sc_b % 4 == 0)) ? 1 : 0;
+    // 32-B aligned rows take 256-bit stores in the tensor-core GEMM's persistent epilogue
+    if (a.c_vec && reinterpret_cast<uintptr_t>(a.C) % 32 == 0 && d->sc_m % 8 == 0 && (d->batch == 1 || d->sc_b % 8 == 0))
+        a.c_vec = 2;
 
     // ---- algorithm: 3xTF32 tensor cores for large fp32 (mul, add) contractions
     const int algo = select_algo(d, M);

@@ -96,7 +96,7 @@ struct TcArgs {
     int m_tiles2, n_tiles2;  // optional second rectangle (blocked L-shaped steps),
     int mt2, nt2;            // its CTAs follow the first rectangle's
     float *C; int64_t sc_m, sc_n;
-    int c_vec;
+    int c_vec;            // 1: 16-B aligned unit-stride C rows (float4 stores), 2: 32-B aligned (STG.256)
     EpiStages epi;
     // fast epilogue (fast_n stages, each "+ bias[n * stride]" if bias != null,
     // then ReLU if relu): set by the host when every stage has that form
@@ -1001,6 +1001,53 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
                         make_float4(tot[bj * 32 + c * 4], tot[bj * 32 + c * 4 + 1], tot[bj * 32 + c * 4 + 2],
                                     tot[bj * 32 + c * 4 + 3]);
                 __syncwarp();
+                if (p.c_vec == 2) {
+                    // 32-B aligned rows: 256-bit stores (STG.256), 8 rows x 128 B
+                    // per instruction -- half the store instructions of the
+                    // float4 form below (C4's per-tile store is what the MMA
+                    // warp waits on)
+                    const int sub8 = lane >> 2, c8 = lane & 3;
+                    const int64_t n8 = n0 + ch * 128 + bj * 32 + c8 * 8;
+                    float fb8[2][8];
+#pragma unroll
+                    for (int i = 0; i < 2; i++)
+#pragma unroll
+                        for (int e = 0; e < 8; e++)
+                            fb8[i][e] = (i < p.fast_n && p.fbias[i] && n8 + e < p.N)
+                                            ? __ldg(p.fbias[i] + (n8 + e) * p.fbias_stride[i])
+                                            : 0.f;
+#pragma unroll 2
+                    for (int i = 0; i < 4; i++) {
+                        const int r = i * 8 + sub8;
+                        const int64_t m = m0 + q * 32 + r;
+                        const float4 v0 = *reinterpret_cast<const float4 *>(blk + r * 32 + (((2 * c8) ^ (r & 7)) * 4));
+                        const float4 v1 = *reinterpret_cast<const float4 *>(blk + r * 32 + (((2 * c8 + 1) ^ (r & 7)) * 4));
+                        if (m >= p.M || n8 >= p.N) continue;
+                        float x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                        for (int j = 0; j < 2; j++) {
+                            if (j >= p.fast_n) break;
+#pragma unroll
+                            for (int e = 0; e < 8; e++) {
+                                if (p.fbias[j]) x[e] += fb8[j][e];
+                                if (p.frelu[j]) x[e] = fmax_nan(x[e], 0.0f);
+                            }
+                        }
+                        float *dst = p.C + m * p.sc_m + n8;
+                        if (n8 + 7 < p.N) {
+                            asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst),
+                                         "f"(x[0]), "f"(x[1]), "f"(x[2]), "f"(x[3]), "f"(x[4]), "f"(x[5]), "f"(x[6]),
+                                         "f"(x[7])
+                                         : "memory");
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 8; e++)
+                                if (n8 + e < p.N) dst[e] = x[e];
+                        }
+                    }
+                    __syncwarp();
+                    continue;
+                }
                 const int64_t n = n0 + ch * 128 + bj * 32 + cc * 4;
                 // host: persistent launches carry no epilogue or the fast one
                 float fb[2][4];
