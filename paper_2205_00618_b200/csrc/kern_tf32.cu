@@ -128,8 +128,12 @@ float *acquire_ws(size_t need, char *err, size_t errlen) {
 // split prepass of one operand viewed as X[r][k] = X[r*s_r + k*s_k] -> hi/lo
 // [R][Kp]: the vectorised kernels when the layout allows, else the scalar one
 // (returns the number of kernels launched)
+// pdl_max: the operand's max pass is launched with programmatic dependent
+// launch (it overlaps the previous kernel, the other operand's split, and its
+// gmax was zeroed by the caller before that split)
 int launch_split(const float *X, int64_t R, int64_t Kd, int64_t s_r, int64_t s_k, float *hi, float *lo, int64_t Kp,
-                 int ilv, int *flag, int *any, int gen, cudaStream_t s, int *gmax = nullptr, int group = 1) {
+                 int ilv, int *flag, int *any, int gen, cudaStream_t s, int *gmax = nullptr, int group = 1,
+                 bool pdl_max = false) {
     const bool small = R * Kp < (1ll << 31) && R * std::max<int64_t>(s_r, 1) + Kd * std::max<int64_t>(s_k, 1) < (1ll << 31);
     const bool al = reinterpret_cast<uintptr_t>(X) % 16 == 0 && Kp % 4 == 0;
     if (ilv && group == 1 && small && al && s_k == 1 && s_r % 4 == 0 && Kd % 4 == 0 && !knobs().scalar_split) {
@@ -141,13 +145,22 @@ int launch_split(const float *X, int64_t R, int64_t Kd, int64_t s_r, int64_t s_k
     if (ilv) {
         // the fp16 cross terms' scale source: finite max |x| per row (A) or
         // per 128-row group of the transposed B (split_exp)
-        cudaMemsetAsync(gmax, 0, sizeof(int) * (size_t)((R + group - 1) / group), s);
+        if (!pdl_max) cudaMemsetAsync(gmax, 0, sizeof(int) * (size_t)((R + group - 1) / group), s);
         if (s_r == 1 && group % 128 == 0 && small && al && R % 4 == 0 && s_k % 4 == 0) {
             const int64_t gblocks = (R + 127) / 128;
             const int64_t kslices = std::max<int64_t>(1, std::min<int64_t>((Kd + 7) / 8, (4 * 148 + gblocks - 1) / gblocks));
             const int64_t kchunk = (Kd + kslices - 1) / kslices;
-            dim3 g((unsigned)gblocks, (unsigned)((Kd + kchunk - 1) / kchunk));
-            tc::split_max_rcontig_kernel<<<g, 256, 0, s>>>(X, (int)R, (int)Kd, (int)s_k, group, (int)kchunk, gmax);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)gblocks, (unsigned)((Kd + kchunk - 1) / kchunk));
+            cfg.blockDim = dim3(256);
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = pdl_max ? 1 : 0;
+            cudaLaunchKernelEx(&cfg, tc::split_max_rcontig_kernel, X, (int)R, (int)Kd, (int)s_k, group, (int)kchunk,
+                               gmax);
         } else if (s_k == 1) {
             const bool vec = reinterpret_cast<uintptr_t>(X) % 16 == 0 && s_r % 4 == 0 && Kd % 4 == 0;
             tc::split_max_kcontig_kernel<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(X, R, Kd, s_r, group, vec ? 1 : 0,
@@ -467,10 +480,14 @@ int tf32x3_gemm(int64_t M, int64_t N, int64_t K, const float *A, int64_t sa_m, i
         bgen = g_bgen;
     }
     {
+        // B's scale maxima are zeroed up front so its max pass can run beside
+        // the A split (programmatic dependent launch, launch_split pdl_max)
+        const bool pdl_b = ilv && !reuse_b;
+        if (pdl_b) cudaMemsetAsync(bmax, 0, sizeof(int) * (size_t)((N + tc::kBScaleCols - 1) / tc::kBScaleCols), s);
         int n = launch_split(A, M, K, sa_m, sa_k, ahi, alo, Kp, ilv, rowflag, anyflag, agen, s, amax, 1);
         if (!reuse_b)
             n += launch_split(B, N, K, sb_n, sb_k, bhi, blo, Kp, 2 * ilv, colflag, anyflag + 1, bgen, s, bmax,
-                              tc::kBScaleCols);
+                              tc::kBScaleCols, pdl_b);
         if (aux_launches) *aux_launches = n;
     }
     tc::TcArgs a;

@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(256) split_max_kcontig_kernel(const float *__r
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0 && m > 0.0f) atomicMax(gmax + r / group, __float_as_int(m));
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // see split_max_rcontig_kernel
 }
 
 __global__ void __launch_bounds__(256) split_max_rows_kernel(const float *__restrict__ X, int64_t R, int64_t Kd,
@@ -439,6 +440,7 @@ __global__ void __launch_bounds__(256) split_max_rows_kernel(const float *__rest
     } else if (r < R && m > 0.0f) {
         atomicMax(gmax + r / group, __float_as_int(m));
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // see split_max_rcontig_kernel
 }
 
 // X element (r, k) = X[r*s_r + k*s_k]  ->  hi/lo[r][k] (row-major, Kp columns,
@@ -611,6 +613,11 @@ __global__ void __launch_bounds__(256) split_max_rcontig_kernel(const float *__r
         for (int i = 1; i < 8; i++) m = fmaxf(m, wm[i]);
         if (m > 0.0f) atomicMax(gmax + (blockIdx.x * 128) / group, __float_as_int(m));
     }
+    // launched with programmatic dependent launch right after the A operand's
+    // split, this pass runs beside it; it completes only once that split has
+    // (no-op without a programmatic predecessor), so whatever waits for this
+    // grid also sees the A split
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 __global__ void __launch_bounds__(256) tf32_split_rcontig_kernel(const float *__restrict__ X, int R, int Kd, int s_k,
