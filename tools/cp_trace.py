@@ -16,6 +16,7 @@ with open(sys.argv[1]) as f:
         else:
             rows.append([int(x) for x in line.split()])
 a = np.array(rows, dtype=np.float64)
+a = a[a[:, 62] > 0] if (a[:, 62] > 0).any() else a     # CTAs that ran
 a_raw = a.copy()
 g0, g1 = a[:, 62].copy(), a[:, 61].copy()
 if (a[:, 60] > 0).all():
