@@ -540,13 +540,19 @@ def _execute_row_streamed(kernel, r: "Runner", dev, hosts, buffers, rows) -> int
     return launches
 
 
-#: blocked 3xTF32 schedule: pieces per operand (A rows, B columns), K/1024
-#: clamped to [4, 16] -- long reductions are compute-bound and gain from an
-#: early start (C5: 16 pieces, 53.3 ms vs 54.3 with 8), short ones are
-#: download-bound and lose to per-piece overheads (C4: 4 pieces, 1.9 ms vs
-#: 2.0 with 8 and 2.6 with 16; tools/blocked_timeline.py).  Piece sizes are
-#: multiples of 256 (the widest output tile).  None = that rule.
+#: blocked tensor-core GEMM schedule.  Short reductions (K < 4096) are
+#: download-bound: A row and B column pieces interleave, K/1024 clamped to
+#: [4, 16] of each (C4: 4 pieces, 1.7 ms; 8 and 16 are no better).  Long
+#: ones upload B whole first, then A in K/512 (<= 32) row pieces, each
+#: computed as a full row strip as it lands: output (and its download) then
+#: grows linearly instead of as the growing L of the interleaved order,
+#: whose last L left ~3 ms of download after the compute (C5 e2e: 47.2 ms
+#: interleaved, 44.8 B-first with 16 pieces, 44.1 with 32;
+#: tools/dbg/e2e_order.py, tools/blocked_timeline.py).  Piece sizes are
+#: multiples of 256 (the widest output tile).  BLOCK_PIECES overrides the
+#: piece count.
 BLOCK_PIECES = None
+BLOCK_B_FIRST_K = 4096
 _block_gen = [1 << 30]     # sequence ids, disjoint from the library's per-call stamps
 
 
@@ -583,18 +589,20 @@ def _blocked_plan(kernel: CompiledKernel, r: "Runner", dev, hosts: dict):
     if native.gemm_algo(d) != "tf32x3":
         return None
 
-    npieces = BLOCK_PIECES or max(4, min(16, K // 1024))
+    b_first = K >= BLOCK_B_FIRST_K
+    npieces = BLOCK_PIECES or (max(4, min(32, K // 512)) if b_first else max(4, min(16, K // 1024)))
 
     def pieces(n):
         per = -(-(-(-n // npieces)) // 256) * 256
         return [(x, min(n, x + per)) for x in range(0, n, per)]
     return dict(M=M, N=N, K=K, a=aref.key, b=bref.key, c=cref.key, b_rowmajor=b_rowmajor,
-                rows=pieces(M), cols=pieces(N))
+                rows=pieces(M), cols=[(0, N)] if b_first else pieces(N))
 
 
 def _execute_blocked(kernel, r: "Runner", dev, hosts, buffers, bp) -> int:
     """Copy/compute overlap over both operands: A row pieces and B column
-    pieces cross PCIe interleaved (A0 B0 A1 B1 ...); each is split into the
+    pieces cross PCIe interleaved (A0 B0 A1 B1 ...; for long reductions B is
+    one piece, so the order is A0 B A1 A2 ...); each is split into the
     resident 3xTF32 workspace as it lands (PREP_A / PREP_B), and as soon as
     pieces i of A and B are both resident the new L of the output -- rows
     [0, i] x column piece i, then row piece i x columns [0, i) -- is computed

@@ -1,7 +1,9 @@
 """The blocked 3xTF32 schedule of `execute` (backend._execute_blocked): A row
 pieces and B column pieces split into the resident workspace as they land
 (LSB_GEMM_PREP_A / PREP_B), output rectangles computed from what is split
-(LSB_GEMM_PRESPLIT) and copied back as pitched rectangles.
+(LSB_GEMM_PRESPLIT) and copied back as pitched rectangles -- interleaved
+(A0 B0 A1 B1 ...) or, for long reductions, B whole first and full row
+strips per A piece (BLOCK_B_FIRST_K, forced here with b_first).
 
 The schedule normally starts at 2^34 multiply-adds (C4, C5); here the
 threshold is lowered so ragged mid-size problems take it, and each result is
@@ -64,10 +66,12 @@ def _check(got, ref, exact=True):
         assert common.ref_metric(got[fin], ref[fin]) <= 1e-4
 
 
+@pytest.mark.parametrize("b_first", [False, True], ids=["interleaved", "b_first"])
 @pytest.mark.parametrize("normal", [False, True], ids=["int", "normal"])
 @pytest.mark.parametrize("shape", [(1000, 300, 1300), (512, 77, 512), (2304, 129, 700), (700, 1000, 2600)])
-def test_blocked_mul_add(shape, normal, monkeypatch):
+def test_blocked_mul_add(shape, normal, b_first, monkeypatch):
     calls = _blocked(monkeypatch)
+    monkeypatch.setattr(backend, "BLOCK_B_FIRST_K", 0 if b_first else 1 << 40)
     m, kk, n = shape
     gj = _graph("semiring_mul_add", m=m, k=kk, n=n)
     k = backend.compile_graph(gj)
@@ -76,7 +80,7 @@ def test_blocked_mul_add(shape, normal, monkeypatch):
     backend.execute(k, bufs)
     assert len(calls) == 1, "blocked schedule not taken"
     bp = calls[0]
-    assert len(bp["rows"]) > 1 and len(bp["cols"]) > 1
+    assert len(bp["rows"]) > 1 and (len(bp["cols"]) == 1 if b_first else len(bp["cols"]) > 1)
     ref = O.reference_eval(gj, ins)
     out, = ref
     _check(bufs[out], ref[out], exact=not normal)
@@ -100,10 +104,12 @@ def test_blocked_bias_relu_epilogue(monkeypatch):
         _check(bufs[s], ref[s], exact=False)
 
 
-def test_blocked_nonfinite_late_pieces(monkeypatch):
+@pytest.mark.parametrize("b_first", [False, True], ids=["interleaved", "b_first"])
+def test_blocked_nonfinite_late_pieces(b_first, monkeypatch):
     """inf/NaN in the last A row piece and a middle B column piece: only the
     rectangles computed after those pieces land see the flags."""
     calls = _blocked(monkeypatch)
+    monkeypatch.setattr(backend, "BLOCK_B_FIRST_K", 0 if b_first else 1 << 40)
     m, kk, n = 1280, 96, 1536
     gj = _graph("semiring_mul_add", m=m, k=kk, n=n)
     k = backend.compile_graph(gj)
