@@ -141,6 +141,45 @@ int launch_maxplus_fixup(int reduce, const GemmArgs &a, int ctas, float4 *part, 
     return e == cudaSuccess ? 0 : -1;
 }
 
+// the one-CTA-per-SM variant (maxplus_duo_kernel): two groups per CTA share
+// a segment's slices (bk deep) dynamically; returns the CTA count used, or -1
+template <int BK>
+static int duo_ctas(int64_t units) {
+    static int occ = -1;
+    if (occ < 0) {
+        for (auto fn : {maxplus_duo_kernel<LSB_OP_MAX, BK>, maxplus_duo_kernel<LSB_OP_MIN, BK>})
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DuoCfg<BK>::kSmemBytes);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, maxplus_duo_kernel<LSB_OP_MAX, BK>, kDuoThreads,
+                                                          DuoCfg<BK>::kSmemBytes) != cudaSuccess)
+            occ = 0;
+    }
+    return (int)std::min<int64_t>(units, (int64_t)occ * device_sms());
+}
+int maxplus_duo_ctas(int64_t units, int bk) { return bk == 8 ? duo_ctas<8>(units) : duo_ctas<16>(units); }
+
+template <int BK>
+static int launch_duo(int reduce, const GemmArgs &a, int ctas, float4 *part, int *flags, int epoch, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3(kDuoThreads);
+    cfg.dynamicSmemBytes = DuoCfg<BK>::kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = reduce == LSB_OP_MAX
+                        ? cudaLaunchKernelEx(&cfg, maxplus_duo_kernel<LSB_OP_MAX, BK>, a, part, flags, epoch)
+                        : cudaLaunchKernelEx(&cfg, maxplus_duo_kernel<LSB_OP_MIN, BK>, a, part, flags, epoch);
+    return e == cudaSuccess ? 0 : -1;
+}
+int launch_maxplus_duo(int reduce, const GemmArgs &a, int bk, int ctas, float4 *part, int *flags, int epoch,
+                       cudaStream_t s) {
+    return bk == 8 ? launch_duo<8>(reduce, a, ctas, part, flags, epoch, s)
+                   : launch_duo<16>(reduce, a, ctas, part, flags, epoch, s);
+}
+
 void launch_conv_fold(const ConvArgs &a, int64_t n_img, cudaStream_t s) {
     const int64_t total = n_img * a.M * a.N;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);

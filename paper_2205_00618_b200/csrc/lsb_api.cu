@@ -92,8 +92,9 @@ void read_knobs(lsb::Knobs &k) {
         else if (!strcmp(e, "32x128")) k.tc_cfg = 1;
         else if (!strcmp(e, "16x256")) k.tc_cfg = 2;
     }
-    if (const char *e = getenv("LSB_MP_MODE")) k.mp_mode = !strcmp(e, "cluster") ? 1 : !strcmp(e, "streamk") ? 2 : 0;
+    if (const char *e = getenv("LSB_MP_MODE")) k.mp_mode = !strcmp(e, "cluster") ? 1 : !strcmp(e, "streamk") ? 2 : !strcmp(e, "fixup") ? 3 : 0;
     k.fixup_ctas = num("LSB_FIXUP_CTAS");
+    k.duo_bk = num("LSB_DUO_BK") == 8 ? 8 : 16;
     k.mp_cluster = num("LSB_MP_CLUSTER");
     k.streamk_ctas = num("LSB_STREAMK_CTAS");
     k.conv_splits = num("LSB_CONV_SPLITS");
@@ -568,6 +569,26 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
             // slice count); LSB_MP_MODE=cluster|streamk selects the others
             const int mode = lsb::knobs().mp_mode;
             if (fast && mode == 0) {
+                // one 512-thread CTA per SM, two groups sharing each segment's
+                // slices dynamically (C2: 0.078 -> see DESIGN 3.2b)
+                const int bk = lsb::knobs().duo_bk;
+                const int64_t units = t128 * (d->K / bk);
+                int ctas = lsb::maxplus_duo_ctas(units, bk);
+                if (lsb::knobs().fixup_ctas > 0) ctas = std::max(1, std::min(ctas, lsb::knobs().fixup_ctas));
+                if (ctas >= 1) {
+                    float4 *part = nullptr;
+                    int *flags = nullptr, epoch = 0;
+                    rc = fixup_buffers(ctas, &part, &flags, &epoch);
+                    if (rc) return rc;
+                    lsb::prof_mark(0, s);
+                    const int lrc = lsb::launch_maxplus_duo(d->reduce, a, bk, ctas, part, flags, epoch, s);
+                    lsb::prof_mark(1, s);
+                    if (lrc) return fail(LSB_ERR_CUDA, "maxplus_duo launch (%d CTAs): %s", ctas,
+                                         cudaGetErrorString(cudaGetLastError()));
+                    return check_launch("maxplus_duo");
+                }
+            }
+            if (fast && mode == 3) {
                 const int64_t units = t128 * (d->K / 16);
                 int ctas = lsb::maxplus_fixup_ctas(units);
                 if (lsb::knobs().fixup_ctas > 0) ctas = std::max(1, std::min(ctas, lsb::knobs().fixup_ctas));

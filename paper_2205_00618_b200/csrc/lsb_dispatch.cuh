@@ -22,8 +22,9 @@ constexpr int kAlgoTf32x3Planar = 4;   // LSB_GEMM_ALGO=tf32x3_planar (convs: th
 struct Knobs {
     int gemm_algo;        // LSB_GEMM_ALGO: LSB_ALGO_AUTO | LSB_ALGO_SIMT | LSB_ALGO_TF32X3 | kAlgoTf32x3Nhwc
     int tc_cfg;           // LSB_TC_CFG: -1 auto, 0 = 16x128, 1 = 32x128, 2 = 16x256
-    int mp_mode;          // LSB_MP_MODE: 0 fixup, 1 cluster, 2 streamk
+    int mp_mode;          // LSB_MP_MODE: 0 duo (default), 1 cluster, 2 streamk, 3 fixup (two CTAs per SM)
     int fixup_ctas, mp_cluster, streamk_ctas, conv_splits;   // 0 = model's choice
+    int duo_bk;           // LSB_DUO_BK: slice depth of the duo max-plus kernel (8 | 16)
     int cp_dbg;           // LSB_CP_DBG: planar conv timing experiments (conv_planar.cuh)
     int cp_ctas;          // LSB_CP_CTAS: planar conv grid size (0 = one CTA per SM)
     int cp_nt;            // LSB_CP_NT: planar conv pixel tile (128 / 192 / 256; 0 = by tile count)
@@ -44,6 +45,9 @@ void launch_streamk(int reduce, const GemmArgs &a, int ctas, cudaStream_t s);   
 void launch_streamk_fast(int reduce, const GemmArgs &a, int ctas, cudaStream_t s);   // 2 launches
 int launch_small_gemm(int combine, int reduce, const GemmArgs &a, int64_t batch, cudaStream_t s);   // -1: no kernel
 int maxplus_fixup_ctas(int64_t units);   // co-resident CTA budget (cooperative launch)
+int maxplus_duo_ctas(int64_t units, int bk);   // one 512-thread CTA per SM (maxplus_duo_kernel), bk = 8 | 16
+int launch_maxplus_duo(int reduce, const GemmArgs &a, int bk, int ctas, float4 *part, int *flags, int epoch,
+                       cudaStream_t s);
 int launch_maxplus_fixup(int reduce, const GemmArgs &a, int ctas, float4 *part, int *flags, int epoch,
                          cudaStream_t s);   // 1 launch
 int launch_maxplus_cluster(int reduce, const GemmArgs &a, int splits, cudaStream_t s);   // 1 launch

@@ -272,6 +272,22 @@ __device__ __forceinline__ int mp_flag_acquire(const int *f) {
     return v;
 }
 
+// Timeline probe (tools/dbg/mp_trace.cu defines LSB_MP_TRACE): thread 0 of
+// every CTA stamps %globaltimer at phase boundaries; nothing in product builds.
+#ifdef LSB_MP_TRACE
+__device__ long long *g_mp_trace;   // [ctas][16]: smid, then (tag << 56 | ns) stamps
+__device__ __forceinline__ void mp_stamp(int &n, int tag) {
+    if (threadIdx.x == 0 && n < 16) {
+        long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_mp_trace[blockIdx.x * 16 + n++] = ((long long)tag << 56) | (t & 0x00ffffffffffffffll);
+    }
+}
+#define MP_STAMP(tag) mp_stamp(mp_tn, tag)
+#else
+#define MP_STAMP(tag)
+#endif
+
 template <int OPR>
 __global__ void __launch_bounds__(kThreads, 2) maxplus_fixup_kernel(const GemmArgs p, float4 *part, int *flags,
                                                                      int epoch) {
@@ -340,6 +356,316 @@ __global__ void __launch_bounds__(kThreads, 2) maxplus_fixup_kernel(const GemmAr
             }
         }
         u = seg_end;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// "duo" fixup kernel: ONE 512-thread CTA per SM, two 256-thread groups.
+//
+// Why (B200 timeline of maxplus_fixup_kernel, tools/dbg/mp_trace.cu): with two
+// 256-thread CTAs per SM and equal ranges the warp scheduler gives one CTA
+// ~65 % of the issue slots, so it finishes its 13.8 slices at ~45 us while the
+// other ends at ~62 us after a solo phase that reaches only ~71 % of the
+// FADD2 + FMNMX3 ceiling (2 warps per scheduler); static weighting of the
+// ranges measured slower (which CTA is favoured is not fixed).  Here both
+// groups work on the SAME segment and pull its slices from a shared-memory
+// counter, each with its own cp.async ring and accumulators, so whichever
+// group the scheduler favours simply takes more slices and both finish within
+// one slice of each other.  At the end of a segment the groups swap halves of
+// their accumulators through shared memory (group g ends up with rows
+// [64 g, 64 g + 64) of the merged tile) and BOTH run the fixup on their half:
+// publish / fold / store use all 512 threads.  Ranges are twice as long as the
+// two-CTA kernel's, so a tile has 2-3 contributors instead of 4-5.
+// Same protocol otherwise (epoch flags, contributors publish before anyone
+// waits, cooperative launch); max/min are exact in any order: bit-identical.
+constexpr int kDuoThreads = 2 * kThreads;
+// slice depth BK (8 or 16): what the groups pull from the counter.  At the end
+// of a segment the faster group waits for the slower one's last slice, so a
+// slice should be short; per-slice cost is one group barrier and one pop.
+template <int BK>
+struct DuoCfg {
+    static constexpr int kStages = BK == 8 ? 5 : 3;
+    static constexpr int kApitch = BK + 4;
+    static constexpr int kStageFloats = kMpBM * kApitch + BK * kMpBN;
+    static constexpr int kRingFloats = kStages * kStageFloats;
+    static constexpr size_t kSmemBytes = sizeof(float) * (2 * kRingFloats) + sizeof(float4) * 16 * kThreads;
+};
+
+__device__ __forceinline__ void mp_group_bar(int g) { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); }
+
+// this group's share of slices [0, nsl) of the segment starting at k0, pulled
+// from *next (shared, zeroed before the call) -- q: this group's staged slice
+// indices (shared, kStages ints).  Every stage of the ring is free on exit.
+template <int OPR, int BK>
+__device__ __forceinline__ void mp_group_slices(const GemmArgs &p, float *ring, int64_t m0, int64_t n0, int64_t k0,
+                                                int nsl, float2 (&acc)[8][4], int *next, volatile int *q, int g) {
+    using Cf = DuoCfg<BK>;
+    constexpr int S = Cf::kStages, kPer = BK / 8;   // 16-B chunks per thread and operand
+    const int t = threadIdx.x & (kThreads - 1), tx = t & 15, ty = t >> 4;
+    // chunk j of this thread: A row (t + 256 j) / (BK / 4), k quad (t + 256 j) % (BK / 4);
+    // B k row (t + 256 j) >> 5, column quad t & 31
+    const float *ga[kPer], *gb[kPer];
+    int sa[kPer], sb[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; j++) {
+        const int c = t + j * kThreads;
+        const int a_row = c / (BK / 4), a_kq = (c % (BK / 4)) * 4;
+        const int b_k = c >> 5, b_nq = (c & 31) * 4;
+        ga[j] = p.A + min(m0 + a_row, p.M - 1) * p.sa_m + k0 + a_kq;
+        gb[j] = p.B + (k0 + b_k) * p.sb_k + min(n0 + b_nq, p.N - 4);
+        sa[j] = a_row * Cf::kApitch + a_kq;
+        sb[j] = kMpBM * Cf::kApitch + b_k * kMpBN + b_nq;
+    }
+    const int64_t b_step = BK * p.sb_k;
+
+    auto issue = [&](int slice, int stage) {
+        float *st = ring + stage * Cf::kStageFloats;
+#pragma unroll
+        for (int j = 0; j < kPer; j++) {
+            cp_async16(st + sa[j], ga[j] + slice * BK);
+            cp_async16(st + sb[j], gb[j] + slice * b_step);
+        }
+    };
+
+    if (t == 0) {
+#pragma unroll
+        for (int s = 0; s < S - 1; s++) q[s] = atomicAdd(next, 1);
+    }
+    mp_group_bar(g);
+#pragma unroll
+    for (int s = 0; s < S - 1; s++) {
+        const int sl = q[s];
+        if (sl < nsl) issue(sl, s);
+        cp_async_commit();
+    }
+    for (int it = 0;; it++) {
+        const int cur = q[it % S];
+        if (cur >= nsl) break;   // pops are monotonic: nothing later is staged either
+        if (t == 0) q[(it + S - 1) % S] = atomicAdd(next, 1);
+        cp_async_wait<S - 2>();
+        mp_group_bar(g);   // slice cur visible to the group; stage (it - 1) % S free; next pop visible
+        {
+            const int nxt = q[(it + S - 1) % S];
+            if (nxt < nsl) issue(nxt, (it + S - 1) % S);
+            cp_async_commit();
+        }
+        const float *As = ring + (it % S) * Cf::kStageFloats;
+        const float *Bs = As + kMpBM * Cf::kApitch;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 2) {
+            float2 a[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+                a[i] = *reinterpret_cast<const float2 *>(As + row_of<8>(ty, i) * Cf::kApitch + kk);
+            float b0[8], b1[8];
+            {
+                const float4 x0 = *reinterpret_cast<const float4 *>(Bs + kk * kMpBN + tx * 4);
+                const float4 x1 = *reinterpret_cast<const float4 *>(Bs + kk * kMpBN + 64 + tx * 4);
+                const float4 y0 = *reinterpret_cast<const float4 *>(Bs + (kk + 1) * kMpBN + tx * 4);
+                const float4 y1 = *reinterpret_cast<const float4 *>(Bs + (kk + 1) * kMpBN + 64 + tx * 4);
+                b0[0] = x0.x; b0[1] = x0.y; b0[2] = x0.z; b0[3] = x0.w;
+                b0[4] = x1.x; b0[5] = x1.y; b0[6] = x1.z; b0[7] = x1.w;
+                b1[0] = y0.x; b1[1] = y0.y; b1[2] = y0.z; b1[3] = y0.w;
+                b1[4] = y1.x; b1[5] = y1.y; b1[6] = y1.z; b1[7] = y1.w;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const float2 s = __fadd2_rn(make_float2(a[i].x, a[i].x), make_float2(b0[2 * j], b0[2 * j + 1]));
+                    const float2 v = __fadd2_rn(make_float2(a[i].y, a[i].y), make_float2(b1[2 * j], b1[2 * j + 1]));
+                    acc[i][j].x = Op<OPR>::apply(acc[i][j].x, Op<OPR>::apply(s.x, v.x));
+                    acc[i][j].y = Op<OPR>::apply(acc[i][j].y, Op<OPR>::apply(s.y, v.y));
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+    mp_group_bar(g);   // every stage free again
+}
+
+// group GI's tail of a segment (GI is the compile-time group index, so the
+// accumulator halves are addressed statically)
+template <int OPR, int GI>
+struct MpDuoTail {
+    static constexpr int kOwn = 4 * GI, kOther = 4 * (1 - GI);
+    // send the other group's rows
+    static __device__ __forceinline__ void send(float4 *xch, int t, const float2 (&acc)[8][4]) {
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+                xch[(GI * 8 + i * 2 + h) * kThreads + t] = make_float4(acc[kOther + i][2 * h].x, acc[kOther + i][2 * h].y,
+                                                                       acc[kOther + i][2 * h + 1].x, acc[kOther + i][2 * h + 1].y);
+    }
+    static __device__ __forceinline__ void fold4(float2 (&acc)[8][4], int i, int h, const float4 w) {
+        acc[kOwn + i][2 * h].x = Op<OPR>::apply(acc[kOwn + i][2 * h].x, w.x);
+        acc[kOwn + i][2 * h].y = Op<OPR>::apply(acc[kOwn + i][2 * h].y, w.y);
+        acc[kOwn + i][2 * h + 1].x = Op<OPR>::apply(acc[kOwn + i][2 * h + 1].x, w.z);
+        acc[kOwn + i][2 * h + 1].y = Op<OPR>::apply(acc[kOwn + i][2 * h + 1].y, w.w);
+    }
+    // fold the rows the other group sent
+    static __device__ __forceinline__ void recv(const float4 *xch, int t, float2 (&acc)[8][4]) {
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) fold4(acc, i, h, xch[((1 - GI) * 8 + i * 2 + h) * kThreads + t]);
+    }
+    // partial tile slots of this group: (kOwn + i) * 2 + h
+    static __device__ __forceinline__ void publish(float4 *dst, int t, const float2 (&acc)[8][4]) {
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+                __stcg(dst + ((kOwn + i) * 2 + h) * kThreads + t,
+                       make_float4(acc[kOwn + i][2 * h].x, acc[kOwn + i][2 * h].y, acc[kOwn + i][2 * h + 1].x,
+                                   acc[kOwn + i][2 * h + 1].y));
+    }
+    static __device__ __forceinline__ void fold_part(const float4 *src, int t, float2 (&acc)[8][4]) {
+        float4 w[8];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) w[i * 2 + h] = __ldcg(src + ((kOwn + i) * 2 + h) * kThreads + t);
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) fold4(acc, i, h, w[i * 2 + h]);
+    }
+    static __device__ __forceinline__ void fold_part2(const float4 *s0, const float4 *s1, int t, float2 (&acc)[8][4]) {
+        float4 w[8], x[8];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                w[i * 2 + h] = __ldcg(s0 + ((kOwn + i) * 2 + h) * kThreads + t);
+                x[i * 2 + h] = __ldcg(s1 + ((kOwn + i) * 2 + h) * kThreads + t);
+            }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                fold4(acc, i, h, w[i * 2 + h]);
+                fold4(acc, i, h, x[i * 2 + h]);
+            }
+    }
+    static __device__ __forceinline__ void store(const GemmArgs &p, int64_t m0, int64_t n0, int tx, int ty,
+                                                 const float2 (&acc)[8][4]) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int64_t m = m0 + row_of<8>(ty, kOwn + i);
+            if (m >= p.M) continue;
+            float *dst = p.C + m * p.sc_m;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int64_t n = n0 + h * 64 + tx * 4;
+                const float v[4] = {acc[kOwn + i][2 * h].x, acc[kOwn + i][2 * h].y, acc[kOwn + i][2 * h + 1].x,
+                                    acc[kOwn + i][2 * h + 1].y};
+                if (p.c_vec && n + 3 < p.N) {
+                    *reinterpret_cast<float4 *>(dst + n) = make_float4(v[0], v[1], v[2], v[3]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (n + q < p.N) dst[(n + q) * p.sc_n] = v[q];
+                }
+            }
+        }
+    }
+};
+
+template <int OPR, int BK>
+__global__ void __launch_bounds__(kDuoThreads, 1) maxplus_duo_kernel(const GemmArgs p, float4 *part, int *flags,
+                                                                      int epoch) {
+    using Cf = DuoCfg<BK>;
+    extern __shared__ __align__(16) float mp_smem[];
+    __shared__ int s_next;
+    __shared__ int s_q[2][Cf::kStages];
+    const int g = threadIdx.x >> 8, t = threadIdx.x & (kThreads - 1), tx = t & 15, ty = t >> 4;
+    float *ring = mp_smem + g * Cf::kRingFloats;
+    float4 *xch = reinterpret_cast<float4 *>(mp_smem + 2 * Cf::kRingFloats);
+    const int64_t n_tiles = (p.N + kMpBN - 1) / kMpBN, m_tiles = (p.M + kMpBM - 1) / kMpBM;
+    const int64_t ks = p.K / BK;
+    const int64_t U = m_tiles * n_tiles * ks, G = gridDim.x, b = blockIdx.x;
+    const int64_t u0 = U * b / G, u1 = U * (b + 1) / G;
+#ifdef LSB_MP_TRACE
+    int mp_tn = 1;
+    if (threadIdx.x == 0) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_mp_trace[b * 16] = sm;
+    }
+#endif
+    MP_STAMP(1);   // start
+    bool release_due = false;   // partial stored, flag not yet released (uniform)
+    for (int64_t u = u0; u < u1;) {
+        const int64_t tile = u / ks, s0 = u % ks, tile_end = (tile + 1) * ks;
+        const int64_t seg_end = min(u1, tile_end);
+        const int64_t m0 = (tile / n_tiles) * kMpBM, n0 = (tile % n_tiles) * kMpBN;
+        if (threadIdx.x == 0) s_next = 0;
+        __syncthreads();   // also: the previous segment's exchange reads and partial stores are done
+        if (release_due) {
+            // the previous segment's partial: every thread's stores precede the
+            // barrier above, so thread 0's release publishes them all.  Done
+            // here, not right after the stores: the release waits for the
+            // stores to land (~1-2 us) and only delays thread 0's group, whose
+            // slices the other group picks up meanwhile.
+            if (threadIdx.x == 0) mp_flag_release(flags + b, epoch);
+            release_due = false;
+            MP_STAMP(3);   // published
+        }
+        float2 acc[8][4];
+        mp_acc_init<OPR>(acc);
+        mp_group_slices<OPR, BK>(p, ring, m0, n0, s0 * BK, (int)(seg_end - u), acc, &s_next, s_q[g], g);
+        MP_STAMP(2);   // group 0's slices done
+        if (g == 0) MpDuoTail<OPR, 0>::send(xch, t, acc);
+        else MpDuoTail<OPR, 1>::send(xch, t, acc);
+        __syncthreads();
+        if (g == 0) MpDuoTail<OPR, 0>::recv(xch, t, acc);
+        else MpDuoTail<OPR, 1>::recv(xch, t, acc);
+        MP_STAMP(6);   // halves merged
+        if (s0 != 0) {
+            // contributor: this CTA's (only) partial tile, thread-major float4s
+            float4 *dst = part + b * (16 * kThreads);
+            if (g == 0) MpDuoTail<OPR, 0>::publish(dst, t, acc);
+            else MpDuoTail<OPR, 1>::publish(dst, t, acc);
+            release_due = true;
+        } else {
+            // owner: fold the partials of the later CTAs reaching into the tile,
+            // two at a time when both are already published
+            int64_t c = b + 1;
+            int nc = 0;
+            if (seg_end < tile_end)
+                while (c + nc < G && U * (c + nc) / G < tile_end) nc++;
+            while (nc > 0) {
+                if (threadIdx.x == 0) {
+                    while (mp_flag_acquire(flags + c) != epoch) __nanosleep(32);
+                    s_next = (nc > 1 && mp_flag_acquire(flags + c + 1) == epoch) ? 2 : 1;
+                }
+                __syncthreads();
+                const int r = s_next;
+                __syncthreads();   // everyone has read it: thread 0 may rewrite s_next
+                MP_STAMP(4);   // r contributors ready
+                const float4 *src = part + c * (16 * kThreads);
+                if (r == 2) {
+                    if (g == 0) MpDuoTail<OPR, 0>::fold_part2(src, src + 16 * kThreads, t, acc);
+                    else MpDuoTail<OPR, 1>::fold_part2(src, src + 16 * kThreads, t, acc);
+                } else {
+                    if (g == 0) MpDuoTail<OPR, 0>::fold_part(src, t, acc);
+                    else MpDuoTail<OPR, 1>::fold_part(src, t, acc);
+                }
+                c += r;
+                nc -= r;
+            }
+            if (g == 0) MpDuoTail<OPR, 0>::store(p, m0, n0, tx, ty, acc);
+            else MpDuoTail<OPR, 1>::store(p, m0, n0, tx, ty, acc);
+            MP_STAMP(5);   // tile stored
+        }
+        u = seg_end;
+    }
+    if (release_due) {
+        __syncthreads();
+        if (threadIdx.x == 0) mp_flag_release(flags + b, epoch);
+        MP_STAMP(3);
     }
 }
 

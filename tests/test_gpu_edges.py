@@ -259,15 +259,19 @@ def test_tropical_split_k_paths(op, shape):
     _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
 
 
-@pytest.mark.parametrize("mode", ["fixup", "cluster", "streamk"])
+@pytest.mark.parametrize("mode", ["duo", "duo:8", "fixup", "cluster", "streamk"])
 @pytest.mark.parametrize("op,shape", [("add_max", (1024, 1024, 1024)), ("add_min", (777, 1040, 1000)),
-                                      ("add_max", (130, 4096, 260))])
+                                      ("add_max", (130, 4096, 260)), ("add_min", (2048, 512, 1100))])
 def test_tropical_underfilled_modes(mode, op, shape, monkeypatch):
-    """The three kernels for underfilled (add, max|min) grids -- stream-K with
-    the in-kernel fixup (default), cluster split-K with DSMEM folds, stream-K
-    with atomic merges (LSB_MP_MODE) -- give the same bytes as the reference,
-    NaN / inf included, wherever the partial boundaries fall."""
-    monkeypatch.setenv("LSB_MP_MODE", mode)
+    """The kernels for underfilled (add, max|min) grids -- stream-K with the
+    in-kernel fixup as one 512-thread CTA per SM whose two groups pull slices
+    from a shared counter (duo, the default; 16- or 8-deep slices) or as two
+    CTAs per SM (fixup), cluster split-K with DSMEM folds, stream-K with
+    atomic merges (LSB_MP_MODE) -- give the same bytes as the reference, NaN /
+    inf included, wherever the partial boundaries fall."""
+    monkeypatch.setenv("LSB_MP_MODE", mode.split(":")[0])
+    if ":" in mode:
+        monkeypatch.setenv("LSB_DUO_BK", mode.split(":")[1])
     m, k, n = shape
     gj = _graph(f"semiring_{op}", m=m, k=k, n=n)
     kern, ins = _inputs(gj, 41, -50, 51)
