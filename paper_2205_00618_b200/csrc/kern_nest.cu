@@ -1,9 +1,116 @@
 // kern_nest.cu -- general affine loop-nest kernels, one per operator pair.
 #include <algorithm>
+#include <climits>
+#include <cstring>
 
 #include "lsb_dispatch.cuh"
+#include "nest_fast.cuh"
 
 namespace lsb {
+
+// ---- fast path (nest_fast.cuh) ---------------------------------------------
+namespace {
+// |base| + sum |coeff| (extent - 1) of an affine form over the padded dims, or -1 past 31 bits
+bool pack_affine(const lsb_nest_desc &d, const lsb_affine &f, NfAffine *out) {
+    const int so = kNfOut - d.n_out, sr = kNfRed - d.n_red;
+    int64_t span = f.base < 0 ? -f.base : f.base;
+    memset(out, 0, sizeof(*out));
+    for (int i = 0; i < d.n_out + d.n_red; i++) {
+        const int64_t c = f.coeff[i];
+        span += (c < 0 ? -c : c) * (d.extent[i] - 1);
+        if (c > INT32_MAX || c < INT32_MIN) return false;
+        if (i < d.n_out) out->co[so + i] = (int)c;
+        else out->cr[sr + i - d.n_out] = (int)c;
+    }
+    if (span >= INT32_MAX || f.base > INT32_MAX || f.base < INT32_MIN) return false;
+    out->base = (int)f.base;
+    return true;
+}
+
+template <int NOPS, bool GUARDS, bool RED>
+void launch_rows(const NestFastArgs &a, dim3 grid, int tx_log2, cudaStream_t s) {
+    nest_rows_kernel<NOPS, GUARDS, RED><<<grid, 256, 0, s>>>(a, tx_log2);
+}
+}  // namespace
+
+int launch_nest_fast(const lsb_nest_desc &d, const EpiStages &epi, cudaStream_t s) {
+    if (d.n_out > kNfOut || d.n_red > kNfRed || d.n_operands > kNfOps) return 0;
+    NestFastArgs a;
+    memset(&a, 0, sizeof(a));
+    const int so = kNfOut - d.n_out, sr = kNfRed - d.n_red;
+    int64_t points = 1, red = 1;
+    for (int i = 0; i < kNfOut; i++) a.eo[i] = 1;
+    for (int i = 0; i < kNfRed; i++) a.er[i] = 1;
+    for (int i = 0; i < d.n_out + d.n_red; i++) {
+        if (d.extent[i] >= INT32_MAX) return 0;
+        if (i < d.n_out) { a.eo[so + i] = (int)d.extent[i]; points *= d.extent[i]; }
+        else { a.er[sr + i - d.n_out] = (int)d.extent[i]; red *= d.extent[i]; }
+    }
+    if (points >= INT32_MAX || red >= INT32_MAX) return 0;
+    a.shift = so;
+    a.n_rows = a.eo[0] * a.eo[1] * a.eo[2];
+    bool guards = false;
+    for (int o = 0; o < d.n_operands; o++) {
+        const lsb_nest_operand &src = d.operand[o];
+        if (src.n_guards > kNfGuards) return 0;
+        a.op[o].ptr = src.ptr;
+        a.op[o].fill = src.fill;
+        a.op[o].n_guards = src.n_guards;
+        if (!pack_affine(d, src.addr, &a.op[o].addr)) return 0;
+        for (int q = 0; q < src.n_guards; q++) {
+            if (!pack_affine(d, src.guard[q], &a.op[o].guard[q])) return 0;
+            if (src.guard_size[q] < 0 || src.guard_size[q] > INT32_MAX) return 0;
+            a.op[o].guard_size[q] = (unsigned)src.guard_size[q];
+            guards = true;
+        }
+    }
+    if (!pack_affine(d, d.out_addr, &a.out_addr)) return 0;
+    a.out = d.out;
+    a.beta = d.beta;
+    a.combine = d.combine;
+    a.reduce = d.reduce;
+    a.epi = epi;
+    const int inner = a.eo[3];
+    // permutation of a single operand: 32 x 32 smem tiles
+    if (d.n_red == 0 && d.n_operands == 1 && !guards && epi.n == 0 && d.beta == 1.0f && a.out_addr.co[3] == 1 &&
+        a.op[0].addr.co[3] != 1 && inner >= 16) {
+        int q = -1;
+        for (int i = 0; i < 3; i++)
+            if (a.op[0].addr.co[i] == 1 && a.eo[i] >= 16) q = i;
+        if (q >= 0) {
+            a.tq = q;
+            a.tb0 = q == 0 ? 1 : 0;
+            a.tb1 = q == 2 ? 1 : 2;
+            const int64_t batch = (int64_t)a.eo[a.tb0] * a.eo[a.tb1];
+            dim3 grid((unsigned)((inner + 31) / 32), (unsigned)((a.eo[q] + 31) / 32),
+                      (unsigned)std::min<int64_t>(batch, 65535));
+            if (grid.y <= 65535) {
+                nest_transpose_kernel<<<grid, 256, 0, s>>>(a);
+                return 2;
+            }
+        }
+    }
+    int tx_log2 = 3;
+    while (tx_log2 < 8 && (1 << tx_log2) < inner) tx_log2++;
+    const int TX = 1 << tx_log2, TY = 256 >> tx_log2;
+    const int64_t row_blocks = ((int64_t)a.n_rows + TY - 1) / TY;
+    int64_t gx = ((int64_t)inner + 4 * TX - 1) / (4 * TX);
+    if (gx * row_blocks < 4 * (int64_t)device_sms()) gx = ((int64_t)inner + TX - 1) / TX;
+    dim3 grid((unsigned)gx, (unsigned)std::min<int64_t>(row_blocks, 65535));
+    const bool red_loop = d.n_red > 0;
+    const int key = (d.n_operands == 2 ? 4 : 0) | (guards ? 2 : 0) | (red_loop ? 1 : 0);
+    switch (key) {
+    case 0: launch_rows<1, false, false>(a, grid, tx_log2, s); break;
+    case 1: launch_rows<1, false, true>(a, grid, tx_log2, s); break;
+    case 2: launch_rows<1, true, false>(a, grid, tx_log2, s); break;
+    case 3: launch_rows<1, true, true>(a, grid, tx_log2, s); break;
+    case 4: launch_rows<2, false, false>(a, grid, tx_log2, s); break;
+    case 5: launch_rows<2, false, true>(a, grid, tx_log2, s); break;
+    case 6: launch_rows<2, true, false>(a, grid, tx_log2, s); break;
+    default: launch_rows<2, true, true>(a, grid, tx_log2, s); break;
+    }
+    return 1;
+}
 
 template <int C, int R>
 void launch_nest(const NestArgs &a, cudaStream_t s) {

@@ -107,6 +107,7 @@ void read_knobs(lsb::Knobs &k) {
     k.no_persist = on("LSB_NO_PERSIST");
     k.no_fast_epi = on("LSB_NO_FAST_EPI");
     k.no_ilv = on("LSB_NO_ILV");
+    k.no_nest_fast = on("LSB_NO_NEST_FAST");
     k.no_small = on("LSB_NO_SMALL");
     k.no_streamk = on("LSB_NO_STREAMK");
     k.no_mp_fast = on("LSB_NO_MP_FAST");
@@ -795,6 +796,8 @@ int lsb_conv2d_nchw(const lsb_conv_desc *d, void *stream) {
     return check_launch("conv_splitk_fold");
 }
 
+static int g_last_nest_kind = 0;   // lsb_last_nest_kernel (diagnostics)
+
 int lsb_affine_nest(const lsb_nest_desc *d, void *stream) {
     if (!d) return fail(LSB_ERR_INVALID, "null desc");
     if (d->n_out < 0 || d->n_red < 0 || d->n_out + d->n_red > LSB_MAX_NEST_DIMS)
@@ -824,8 +827,14 @@ int lsb_affine_nest(const lsb_nest_desc *d, void *stream) {
     a.out = d->out; a.out_addr = d->out_addr; a.beta = d->beta;
     a.epi = pack_epi(d->n_epi, d->epi);
     if ((rc = check_device())) return rc;
-    kNest[d->combine][d->reduce](a, (cudaStream_t)stream);
+    g_last_nest_kind = lsb::knobs().no_nest_fast ? 0 : lsb::launch_nest_fast(*d, a.epi, (cudaStream_t)stream);
+    if (g_last_nest_kind == 0) kNest[d->combine][d->reduce](a, (cudaStream_t)stream);
     return check_launch("affine_nest");
+}
+
+int lsb_last_nest_kernel(int *kind) {
+    if (kind) *kind = g_last_nest_kind;
+    return LSB_OK;
 }
 
 }  // extern "C"

@@ -29,6 +29,7 @@ struct Knobs {
     int cp_ctas;          // LSB_CP_CTAS: planar conv grid size (0 = one CTA per SM)
     int cp_nt;            // LSB_CP_NT: planar conv pixel tile (128 / 192 / 256; 0 = by tile count)
     bool scalar_split, no_pair, no_tail_split, no_persist, no_fast_epi, no_ilv;
+    bool no_nest_fast;    // LSB_NO_NEST_FAST: every nest through affine_nest_kernel
     bool no_small, no_streamk, no_mp_fast, no_mp_cluster, no_conv_split;
     char gemm_trace[256], conv_trace[256];   // "" = off
 };
@@ -37,6 +38,11 @@ void reload_knobs();
 // optional timing of the dominant kernel of a call (lsb_profile): which = 0
 // before its launch, 1 after; no-op unless profiling is enabled
 void prof_mark(int which, cudaStream_t s);
+
+// the 32-bit row-walking / tiled-transpose nest kernels (nest_fast.cuh):
+// returns 0 when the nest does not qualify (caller runs affine_nest_kernel),
+// 1 = nest_rows_kernel, 2 = nest_transpose_kernel launched
+int launch_nest_fast(const lsb_nest_desc &d, const EpiStages &epi, cudaStream_t s);
 
 GemmFn fast_gemm(int combine, int reduce, int bm, bool two_level);   // kern_fast.cu (nullptr if untuned)
 void launch_conv_fast(const ConvArgs &a, dim3 grid, size_t dyn, cudaStream_t s);

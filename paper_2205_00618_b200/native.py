@@ -118,6 +118,7 @@ _SIGS = {
     "lsb_host_is_pinned": ([vp, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "lsb_last_gemm_launch": ([ctypes.POINTER(ctypes.c_int)] * 4, ctypes.c_int),
     "lsb_last_conv_kernel": ([ctypes.POINTER(ctypes.c_int)] * 2, ctypes.c_int),
+    "lsb_last_nest_kernel": ([ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "lsb_nccl_unique_id": ([ctypes.c_char_p], ctypes.c_int),
     "lsb_nccl_init": ([ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)], ctypes.c_int),
     "lsb_nccl_destroy": ([vp], ctypes.c_int),
@@ -313,6 +314,13 @@ def last_gemm_launch() -> dict:
     v = [ctypes.c_int() for _ in range(4)]
     check(lib().lsb_last_gemm_launch(*(ctypes.byref(x) for x in v)), "lsb_last_gemm_launch")
     return dict(zip(("bn", "ctas", "units", "pair"), (x.value for x in v)))
+
+
+def last_nest_kernel() -> int:
+    """Which kernel the last affine-nest call launched: 0 general, 1 rows, 2 transpose."""
+    k = ctypes.c_int(0)
+    check(lib().lsb_last_nest_kernel(ctypes.byref(k)), "lsb_last_nest_kernel")
+    return k.value
 
 
 def last_conv_kernel() -> tuple:
