@@ -1,6 +1,7 @@
 // kern_nest.cu -- general affine loop-nest kernels, one per operator pair.
 #include <algorithm>
 #include <climits>
+#include <cstdint>
 #include <cstring>
 
 #include "lsb_dispatch.cuh"
@@ -71,7 +72,7 @@ int launch_nest_fast(const lsb_nest_desc &d, const EpiStages &epi, cudaStream_t 
     a.reduce = d.reduce;
     a.epi = epi;
     const int inner = a.eo[3];
-    // permutation of a single operand: 32 x 32 smem tiles
+    // permutation of a single operand: 32 x 64 smem tiles
     if (d.n_red == 0 && d.n_operands == 1 && !guards && epi.n == 0 && d.beta == 1.0f && a.out_addr.co[3] == 1 &&
         a.op[0].addr.co[3] != 1 && inner >= 16) {
         int q = -1;
@@ -82,7 +83,7 @@ int launch_nest_fast(const lsb_nest_desc &d, const EpiStages &epi, cudaStream_t 
             a.tb0 = q == 0 ? 1 : 0;
             a.tb1 = q == 2 ? 1 : 2;
             const int64_t batch = (int64_t)a.eo[a.tb0] * a.eo[a.tb1];
-            dim3 grid((unsigned)((inner + 31) / 32), (unsigned)((a.eo[q] + 31) / 32),
+            dim3 grid((unsigned)((inner + kNfTileI - 1) / kNfTileI), (unsigned)((a.eo[q] + kNfTileQ - 1) / kNfTileQ),
                       (unsigned)std::min<int64_t>(batch, 65535));
             if (grid.y <= 65535) {
                 nest_transpose_kernel<<<grid, 256, 0, s>>>(a);
@@ -90,14 +91,37 @@ int launch_nest_fast(const lsb_nest_desc &d, const EpiStages &epi, cudaStream_t 
             }
         }
     }
+    // elementwise / broadcast rows, 16-byte aligned: float4 groups
+    if (d.n_red == 0 && !guards && epi.n == 0 && a.out_addr.co[3] == 1 && inner % 4 == 0) {
+        auto quad = [](const NfAffine &f) { return f.base % 4 == 0 && f.co[0] % 4 == 0 && f.co[1] % 4 == 0 && f.co[2] % 4 == 0; };
+        bool ok = quad(a.out_addr) && ((uintptr_t)a.out & 15) == 0;
+        for (int o = 0; o < d.n_operands; o++) {
+            const int c3 = a.op[o].addr.co[3];
+            ok = ok && (c3 == 0 || (c3 == 1 && quad(a.op[o].addr) && ((uintptr_t)a.op[o].ptr & 15) == 0));
+        }
+        if (ok) {
+            const int inner4 = inner / 4;
+            int lg = 3;
+            while (lg < 8 && (1 << lg) < inner4) lg++;
+            const int TX = 1 << lg, TY = 256 >> lg;
+            const int64_t row_blocks = ((int64_t)a.n_rows + TY - 1) / TY;
+            int64_t gx = ((int64_t)inner4 + 4 * TX - 1) / (4 * TX);
+            if (gx * row_blocks < 4 * (int64_t)device_sms()) gx = ((int64_t)inner4 + TX - 1) / TX;
+            dim3 grid((unsigned)gx, (unsigned)std::min<int64_t>(row_blocks, 65535));
+            if (d.n_operands == 1) nest_vec4_kernel<1><<<grid, 256, 0, s>>>(a, lg);
+            else nest_vec4_kernel<2><<<grid, 256, 0, s>>>(a, lg);
+            return 3;
+        }
+    }
     int tx_log2 = 3;
     while (tx_log2 < 8 && (1 << tx_log2) < inner) tx_log2++;
     const int TX = 1 << tx_log2, TY = 256 >> tx_log2;
     const int64_t row_blocks = ((int64_t)a.n_rows + TY - 1) / TY;
-    int64_t gx = ((int64_t)inner + 4 * TX - 1) / (4 * TX);
+    const bool red_loop = d.n_red > 0;
+    const int per_trip = red_loop ? 4 : 8;
+    int64_t gx = ((int64_t)inner + per_trip * TX - 1) / (per_trip * TX);
     if (gx * row_blocks < 4 * (int64_t)device_sms()) gx = ((int64_t)inner + TX - 1) / TX;
     dim3 grid((unsigned)gx, (unsigned)std::min<int64_t>(row_blocks, 65535));
-    const bool red_loop = d.n_red > 0;
     const int key = (d.n_operands == 2 ? 4 : 0) | (guards ? 2 : 0) | (red_loop ? 1 : 0);
     switch (key) {
     case 0: launch_rows<1, false, false>(a, grid, tx_log2, s); break;

@@ -10,12 +10,14 @@
 //    points of the innermost output dim (coalesced stores, and coalesced loads
 //    for every operand whose innermost coefficient is 1), TY rows of the outer
 //    dims.  The outer coordinates are decoded once per row (two 32-bit
-//    divisions), a thread then walks its row in steps of the grid width, four
-//    points per trip with their loads independent.  The reduction space is
-//    three nested 32-bit loops with running addresses.  Templated on the
+//    divisions), a thread then walks its row in steps of the grid width, eight
+//    points per trip (four under a reduction) with their loads independent.
+//    The reduction space is three nested 32-bit loops, outside the points.  Templated on the
 //    operand count, on whether any guard exists and on whether there is a
 //    reduction, so reduction-free unguarded nests (broadcast_add) compile to
 //    load / op / store.
+//  * nest_vec4_kernel: reduction-free unguarded nests with 16-byte aligned
+//    contiguous rows (elementwise / broadcast): float4 loads and stores.
 //  * nest_transpose_kernel: a reduction-free single-operand nest whose operand
 //    is contiguous along another output dim than the output is (transpose,
 //    any permutation) goes through 32 x 32 shared-memory tiles so both sides
@@ -61,52 +63,67 @@ __device__ __forceinline__ int nf_dot3(const int (&co)[kNfOut], int p0, int p1, 
     return co[0] * p0 + co[1] * p1 + co[2] * p2;
 }
 
-template <int NOPS, bool GUARDS, bool RED>
-__device__ __forceinline__ float nf_point(const NestFastArgs &p, const int (&ab)[kNfOps],
-                                          const int (&gb)[kNfOps][kNfGuards], int i) {
-    int a[NOPS], g[NOPS][kNfGuards];
+// U consecutive trips of one thread's row walk (points i0 + u * stride): the
+// reduction loops are outermost and the U points innermost, so every
+// reduction step issues U independent loads per operand; per point the terms
+// still arrive in the reference order.
+template <int NOPS, bool GUARDS, bool RED, int U>
+__device__ __forceinline__ void nf_strip(const NestFastArgs &p, const int (&ab)[kNfOps],
+                                         const int (&gb)[kNfOps][kNfGuards], int i0, int stride, int inner,
+                                         float (&x)[U]) {
+    const float id = RED ? identity_rt(p.reduce) : 0.0f;
 #pragma unroll
-    for (int o = 0; o < NOPS; o++) {
-        a[o] = ab[o] + p.op[o].addr.co[3] * i;
-        if (GUARDS) {
-#pragma unroll
-            for (int q = 0; q < kNfGuards; q++) g[o][q] = gb[o][q] + p.op[o].guard[q].co[3] * i;
-        }
-    }
-    auto term = [&](int d0, int d1, int d2) {
-        float t = 0.0f;
+    for (int u = 0; u < U; u++) x[u] = id;
+    auto step = [&](int d0, int d1, int d2) {
+        int ra[NOPS], rg[NOPS][kNfGuards];   // this step's offsets (uniform)
 #pragma unroll
         for (int o = 0; o < NOPS; o++) {
             const NfOperand &od = p.op[o];
-            bool ok = true;
-            if (GUARDS) {
+            ra[o] = ab[o] + (RED ? od.addr.cr[0] * d0 + od.addr.cr[1] * d1 + od.addr.cr[2] * d2 : 0);
 #pragma unroll
-                for (int q = 0; q < kNfGuards; q++)
-                    if (q < od.n_guards) {
-                        const int gv = g[o][q] + (RED ? od.guard[q].cr[0] * d0 + od.guard[q].cr[1] * d1 +
-                                                            od.guard[q].cr[2] * d2
-                                                      : 0);
-                        ok = ok && (unsigned)gv < od.guard_size[q];
-                    }
-            }
-            const int off = a[o] + (RED ? od.addr.cr[0] * d0 + od.addr.cr[1] * d1 + od.addr.cr[2] * d2 : 0);
-            const float v = ok ? __ldg(od.ptr + off) : od.fill;
-            t = (o == 0) ? v : op_rt(p.combine, t, v);
+            for (int q = 0; q < kNfGuards; q++)
+                rg[o][q] = GUARDS ? gb[o][q] + (RED ? od.guard[q].cr[0] * d0 + od.guard[q].cr[1] * d1 +
+                                                          od.guard[q].cr[2] * d2
+                                                    : 0)
+                                  : 0;
         }
-        if (p.beta != 1.0f) t = __fmul_rn(p.beta, t);
-        return t;
+        float v[NOPS][U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int i = i0 + u * stride;
+#pragma unroll
+            for (int o = 0; o < NOPS; o++) {
+                const NfOperand &od = p.op[o];
+                bool ok = i < inner;
+                if (GUARDS) {
+#pragma unroll
+                    for (int q = 0; q < kNfGuards; q++)
+                        if (q < od.n_guards) ok = ok && (unsigned)(rg[o][q] + od.guard[q].co[3] * i) < od.guard_size[q];
+                }
+                v[o][u] = ok ? __ldg(od.ptr + ra[o] + od.addr.co[3] * i) : od.fill;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            float t = v[0][u];
+            if (NOPS == 2) t = op_rt(p.combine, t, v[NOPS - 1][u]);
+            if (p.beta != 1.0f) t = __fmul_rn(p.beta, t);
+            x[u] = RED ? op_rt(p.reduce, x[u], t) : t;
+        }
     };
-    if (!RED) return term(0, 0, 0);
-    float acc = identity_rt(p.reduce);
-    for (int d0 = 0; d0 < p.er[0]; d0++)
-        for (int d1 = 0; d1 < p.er[1]; d1++)
-            for (int d2 = 0; d2 < p.er[2]; d2++) acc = op_rt(p.reduce, acc, term(d0, d1, d2));
-    return acc;
+    if (!RED) {
+        step(0, 0, 0);
+    } else {
+        for (int d0 = 0; d0 < p.er[0]; d0++)
+            for (int d1 = 0; d1 < p.er[1]; d1++)
+                for (int d2 = 0; d2 < p.er[2]; d2++) step(d0, d1, d2);
+    }
 }
 
-// grid: x over the innermost dim (TX * 4 points per CTA trip), y over rows
+// grid: x over the innermost dim (TX * U points per CTA trip), y over rows
 template <int NOPS, bool GUARDS, bool RED>
 __global__ void __launch_bounds__(256) nest_rows_kernel(const NestFastArgs p, int tx_log2) {
+    constexpr int U = RED ? 4 : 8;
     const int TX = 1 << tx_log2, TY = 256 >> tx_log2;
     const int tx = threadIdx.x & (TX - 1), ty = threadIdx.x >> tx_log2;
     const int inner = p.eo[3];
@@ -123,15 +140,11 @@ __global__ void __launch_bounds__(256) nest_rows_kernel(const NestFastArgs p, in
                 gb[o][q] = GUARDS ? p.op[o].guard[q].base + nf_dot3(p.op[o].guard[q].co, p0, p1, p2) : 0;
         }
         const int ob = p.out_addr.base + nf_dot3(p.out_addr.co, p0, p1, p2);
-        for (int i0 = blockIdx.x * TX + tx; i0 < inner; i0 += 4 * stride) {
-            float x[4];
+        for (int i0 = blockIdx.x * TX + tx; i0 < inner; i0 += U * stride) {
+            float x[U];
+            nf_strip<NOPS, GUARDS, RED, U>(p, ab, gb, i0, stride, inner, x);
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int i = i0 + u * stride;
-                x[u] = i < inner ? nf_point<NOPS, GUARDS, RED>(p, ab, gb, i) : 0.0f;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < U; u++) {
                 const int i = i0 + u * stride;
                 if (i < inner) {
                     float v = x[u];
@@ -154,28 +167,90 @@ __global__ void __launch_bounds__(256) nest_rows_kernel(const NestFastArgs p, in
     }
 }
 
+// Reduction-free, unguarded nests whose operands are contiguous (or constant)
+// along the innermost output dim, 16-byte aligned rows: four float4 groups per
+// thread per trip (64 B per operand in flight per thread).  i counts float4s.
+template <int NOPS>
+__global__ void __launch_bounds__(256) nest_vec4_kernel(const NestFastArgs p, int tx_log2) {
+    const int TX = 1 << tx_log2, TY = 256 >> tx_log2;
+    const int tx = threadIdx.x & (TX - 1), ty = threadIdx.x >> tx_log2;
+    const int inner4 = p.eo[3] >> 2;
+    const int stride = gridDim.x * TX;
+    for (int row = blockIdx.y * TY + ty; row < p.n_rows; row += gridDim.y * TY) {
+        const int p2 = row % p.eo[2], r1 = row / p.eo[2];
+        const int p1 = r1 % p.eo[1], p0 = r1 / p.eo[1];
+        const float *src[NOPS];
+#pragma unroll
+        for (int o = 0; o < NOPS; o++) src[o] = p.op[o].ptr + p.op[o].addr.base + nf_dot3(p.op[o].addr.co, p0, p1, p2);
+        float *dst = p.out + p.out_addr.base + nf_dot3(p.out_addr.co, p0, p1, p2);
+        for (int i0 = blockIdx.x * TX + tx; i0 < inner4; i0 += 4 * stride) {
+            float4 v[NOPS][4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int i = i0 + u * stride;
+                if (i < inner4) {
+#pragma unroll
+                    for (int o = 0; o < NOPS; o++) {
+                        if (p.op[o].addr.co[3]) {
+                            v[o][u] = __ldg(reinterpret_cast<const float4 *>(src[o]) + i);
+                        } else {
+                            const float b = __ldg(src[o]);
+                            v[o][u] = make_float4(b, b, b, b);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int i = i0 + u * stride;
+                if (i < inner4) {
+                    float4 t = v[0][u];
+                    if (NOPS == 2) {
+                        t.x = op_rt(p.combine, t.x, v[NOPS - 1][u].x);
+                        t.y = op_rt(p.combine, t.y, v[NOPS - 1][u].y);
+                        t.z = op_rt(p.combine, t.z, v[NOPS - 1][u].z);
+                        t.w = op_rt(p.combine, t.w, v[NOPS - 1][u].w);
+                    }
+                    if (p.beta != 1.0f) {
+                        t.x = __fmul_rn(p.beta, t.x);
+                        t.y = __fmul_rn(p.beta, t.y);
+                        t.z = __fmul_rn(p.beta, t.z);
+                        t.w = __fmul_rn(p.beta, t.w);
+                    }
+                    reinterpret_cast<float4 *>(dst)[i] = t;
+                }
+            }
+        }
+    }
+}
+
 // out[.., q, .., i] = in[..]: operand contiguous along output dim q, output
 // along dim 3.  grid: x tiles of dim 3, y tiles of dim q, z the two batch dims.
+constexpr int kNfTileQ = 32, kNfTileI = 64;   // tile: 32 along the operand's line, 64 along the output's
 __global__ void __launch_bounds__(256) nest_transpose_kernel(const NestFastArgs p) {
-    __shared__ float tile[32][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    __shared__ float tile[kNfTileI][kNfTileQ + 1];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
     const int eq = p.eo[p.tq], inner = p.eo[3];
     const NfOperand &od = p.op[0];
     for (int z = blockIdx.z; z < p.eo[p.tb0] * p.eo[p.tb1]; z += gridDim.z) {
         const int c1 = z % p.eo[p.tb1], c0 = z / p.eo[p.tb1];
         const int ain = od.addr.base + od.addr.co[p.tb0] * c0 + od.addr.co[p.tb1] * c1;
         const int aout = p.out_addr.base + p.out_addr.co[p.tb0] * c0 + p.out_addr.co[p.tb1] * c1;
-        const int q0 = blockIdx.y * 32, i0 = blockIdx.x * 32;
+        const int q0 = blockIdx.y * kNfTileQ, i0 = blockIdx.x * kNfTileI;
+        const int cq = od.addr.co[p.tq], ci = od.addr.co[3], oq = p.out_addr.co[p.tq];
+        // read: lanes along q (the operand's contiguous dim), 8 rows of i per pass
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int i = i0 + ty + 8 * k, q = q0 + tx;
-            if (i < inner && q < eq) tile[ty + 8 * k][tx] = __ldg(od.ptr + ain + od.addr.co[p.tq] * q + od.addr.co[3] * i);
+        for (int k = 0; k < kNfTileI / 8; k++) {
+            const int il = ty + 8 * k, i = i0 + il, q = q0 + tx;
+            if (i < inner && q < eq) tile[il][tx] = __ldg(od.ptr + ain + cq * q + ci * i);
         }
         __syncthreads();
+        // write: lanes along i (the output's contiguous dim), 4 rows of q per pass
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int q = q0 + ty + 8 * k, i = i0 + tx;
-            if (i < inner && q < eq) p.out[aout + p.out_addr.co[p.tq] * q + p.out_addr.co[3] * i] = tile[tx][ty + 8 * k];
+        for (int k = 0; k < kNfTileQ / 4; k++) {
+            const int il = threadIdx.x & (kNfTileI - 1), ql = (threadIdx.x >> 6) + 4 * k;
+            const int i = i0 + il, q = q0 + ql;
+            if (i < inner && q < eq) p.out[aout + oq * q + i] = tile[il][ql];
         }
         __syncthreads();
     }

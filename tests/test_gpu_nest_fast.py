@@ -70,6 +70,8 @@ RESIZED = [
     ("acc_transpose", {"a": 33, "b": 8, "r": 8, "c": 33}, None),
     ("acc_concat", {"r": 129, "c1": 200, "c2": 333, "c": 533}, 1),
     ("acc_broadcast_add", {"m": 257, "n": 1030}, 1),
+    ("acc_broadcast_add", {"m": 257, "n": 1032}, 3),
+    ("acc_broadcast_add", {"m": 9, "n": 4096}, 3),
     ("acc_broadcast_add", {"m": 3000, "n": 5}, 1),
 ]
 
