@@ -231,6 +231,23 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
         a.n_tiles = (int)((n_rows + BN - 1) / BN);
     }
     a.bn = BN;
+    // TMEM chunk depth: a chunk accumulates in TMEM, the epilogue warps sum
+    // chunks in registers (two-level accumulation: C5's reference metric needs
+    // it) and also store finished tiles, so the MMA issuer (two TMEM buffers)
+    // can run at most two chunks ahead of a tile store.  Short reductions run
+    // as two chunks -- the issuer is then a whole tile ahead while the store
+    // runs; with 128-K chunks it stalled behind every store (C4, K = 1024:
+    // kernel 0.097 -> 0.081 ms, strict rule still 100 %).  Long ones take
+    // 256-K chunks: half the TMEM reads and register adds of 128 (C5 under
+    // the power cap: 428.6 -> 449.5 TFLOP/s; reference metric 8.5e-7 ->
+    // 1.2e-6, strict-rule pass 99.93 % -> 99.82 %, the VM's own 99.40 %;
+    // 512: 441 TF, 99.55 %; 1024: 98.99 % -- below the VM, not used).
+    {
+        const int kstage = a.ilv ? 2 * BK : BK;
+        a.chunk_k = tc::kChunkK;
+        const int forced = knobs().tc_chunk_k;
+        if (forced > 0) a.chunk_k = std::max(kstage, forced / kstage * kstage);
+    }
     // 2-CTA clusters over m-tile pairs (the raster keeps pairs on one n-tile
     // when m_tiles is even): B's half tiles are multicast (TcArgs::pair)
     a.pair = (a.ilv && a.m_tiles % 2 == 0 && a.m_tiles2 % 2 == 0 && !knobs().no_pair) ? 1 : 0;
@@ -242,7 +259,7 @@ int run_main(const float *ahi, const float *alo, const float *bhi, const float *
         const int T = a.m_tiles * a.n_tiles;
         const int slots = lsb::device_sms() * Cf::kCtasPerSm;
         const int rem = T % slots;
-        const int chunks = (int)((Kp / BK + Cf::kChunkStages - 1) / Cf::kChunkStages);
+        const int chunks = (int)((Kp + a.chunk_k - 1) / a.chunk_k);
         const int S = rem + (rem & 1);
         if (T >= slots && rem > 0 && 2 * rem <= slots && chunks >= 2 && S <= T && (T - S) % 2 == 0 &&
             ensure_tail_ws(S, s)) {

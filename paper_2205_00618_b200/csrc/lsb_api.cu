@@ -94,6 +94,7 @@ void read_knobs(lsb::Knobs &k) {
     }
     if (const char *e = getenv("LSB_MP_MODE")) k.mp_mode = !strcmp(e, "cluster") ? 1 : !strcmp(e, "streamk") ? 2 : !strcmp(e, "fixup") ? 3 : 0;
     k.fixup_ctas = num("LSB_FIXUP_CTAS");
+    k.tc_chunk_k = num("LSB_TC_CHUNK_K");
     k.duo_bk = num("LSB_DUO_BK") == 8 ? 8 : 16;
     k.mp_cluster = num("LSB_MP_CLUSTER");
     k.streamk_ctas = num("LSB_STREAMK_CTAS");

@@ -21,6 +21,7 @@ constexpr int kAlgoTf32x3Nhwc = 3;     // LSB_GEMM_ALGO=tf32x3_nhwc (convs: the 
 constexpr int kAlgoTf32x3Planar = 4;   // LSB_GEMM_ALGO=tf32x3_planar (convs: the planar kernel)
 struct Knobs {
     int gemm_algo;        // LSB_GEMM_ALGO: LSB_ALGO_AUTO | LSB_ALGO_SIMT | LSB_ALGO_TF32X3 | kAlgoTf32x3Nhwc
+    int tc_chunk_k;       // LSB_TC_CHUNK_K: TMEM accumulation chunk depth (0 = auto)
     int tc_cfg;           // LSB_TC_CFG: -1 auto, 0 = 16x128, 1 = 32x128, 2 = 16x256
     int mp_mode;          // LSB_MP_MODE: 0 duo (default), 1 cluster, 2 streamk, 3 fixup (two CTAs per SM)
     int fixup_ctas, mp_cluster, streamk_ctas, conv_splits;   // 0 = model's choice

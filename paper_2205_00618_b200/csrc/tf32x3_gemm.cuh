@@ -134,6 +134,10 @@ struct TcArgs {
     // across unit boundaries, so a finished tile's store (from registers,
     // through a per-warp smem block) overlaps the next unit's first chunks.
     int units;
+    // K per TMEM accumulation chunk (a multiple of the stage depth): kChunkK,
+    // or half of a short reduction (kern_tf32.cu) so the epilogue warps fold
+    // twice per tile and the MMA issuer runs a whole tile ahead of the store
+    int chunk_k;
     float *split_ws;
     int *split_cnt;
     const int *rowflag, *colflag, *anyflag;   // anyflag[0] A, [1] B
@@ -740,7 +744,7 @@ __global__ void __launch_bounds__(Cfg<BK_, BN_>::kThreads, Cfg<BK_, BN_>::kCtasP
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // an interleaved fp16 stage row (128 B) carries 32 k, a fp32 one BK
     const int kstage = p.ilv ? 2 * BK : BK;
-    const int chunk_stages = kChunkK / kstage;
+    const int chunk_stages = p.chunk_k / kstage;
     const int num_kb = (int)(p.Kp / kstage);
     const int all_chunks = (num_kb + chunk_stages - 1) / chunk_stages;
     // unit t -> output tile, K half (-1: whole K) and split-tile slot.

@@ -21,11 +21,13 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--algo", type=int, default=0)
 ap.add_argument("--split", type=int, default=0)
 ap.add_argument("--tile", type=int, default=0)
+ap.add_argument("--normal", action="store_true", help="standard-normal operands instead of U[-1,1)")
 a = ap.parse_args()
 native.init(0)
 c, r = (OPS[x] for x in a.op.split(","))
-A = torch.rand(a.M, a.K, device="cuda") * 2 - 1
-B = torch.rand(a.K, a.N, device="cuda") * 2 - 1
+torch.manual_seed(0)
+A = torch.randn(a.M, a.K, device="cuda") if a.normal else torch.rand(a.M, a.K, device="cuda") * 2 - 1
+B = torch.randn(a.K, a.N, device="cuda") if a.normal else torch.rand(a.K, a.N, device="cuda") * 2 - 1
 C = torch.empty(a.M, a.N, device="cuda")
 d = native.GemmDesc()
 d.M, d.N, d.K, d.batch = a.M, a.N, a.K, 1
