@@ -91,8 +91,8 @@ int launch_nest_fast(const lsb_nest_desc &d, const EpiStages &epi, cudaStream_t 
             }
         }
     }
-    // elementwise / broadcast rows, 16-byte aligned: float4 groups
-    if (d.n_red == 0 && !guards && epi.n == 0 && a.out_addr.co[3] == 1 && inner % 4 == 0) {
+    // elementwise / broadcast / concat rows, 16-byte aligned: float4 groups
+    if (d.n_red == 0 && epi.n == 0 && a.out_addr.co[3] == 1 && inner % 4 == 0) {
         auto quad = [](const NfAffine &f) { return f.base % 4 == 0 && f.co[0] % 4 == 0 && f.co[1] % 4 == 0 && f.co[2] % 4 == 0; };
         bool ok = quad(a.out_addr) && ((uintptr_t)a.out & 15) == 0;
         for (int o = 0; o < d.n_operands; o++) {
@@ -108,9 +108,35 @@ int launch_nest_fast(const lsb_nest_desc &d, const EpiStages &epi, cudaStream_t 
             int64_t gx = ((int64_t)inner4 + 4 * TX - 1) / (4 * TX);
             if (gx * row_blocks < 4 * (int64_t)device_sms()) gx = ((int64_t)inner4 + TX - 1) / TX;
             dim3 grid((unsigned)gx, (unsigned)std::min<int64_t>(row_blocks, 65535));
-            if (d.n_operands == 1) nest_vec4_kernel<1><<<grid, 256, 0, s>>>(a, lg);
-            else nest_vec4_kernel<2><<<grid, 256, 0, s>>>(a, lg);
+            if (d.n_operands == 1) {
+                if (guards) nest_vec4_kernel<1, true><<<grid, 256, 0, s>>>(a, lg);
+                else nest_vec4_kernel<1, false><<<grid, 256, 0, s>>>(a, lg);
+            } else {
+                if (guards) nest_vec4_kernel<2, true><<<grid, 256, 0, s>>>(a, lg);
+                else nest_vec4_kernel<2, false><<<grid, 256, 0, s>>>(a, lg);
+            }
             return 3;
+        }
+    }
+    // non-overlapping pooling along the innermost dim, 16-byte aligned rows
+    if (d.n_red > 0 && d.n_operands == 1 && !guards && epi.n == 0 && a.out_addr.co[3] == 1 && inner % 4 == 0 &&
+        a.op[0].addr.cr[2] == 1 && a.er[2] == a.op[0].addr.co[3] && (a.er[2] == 2 || a.er[2] == 4)) {
+        auto quad = [](const NfAffine &f) {
+            return f.base % 4 == 0 && f.co[0] % 4 == 0 && f.co[1] % 4 == 0 && f.co[2] % 4 == 0 && f.cr[0] % 4 == 0 &&
+                   f.cr[1] % 4 == 0;
+        };
+        if (quad(a.out_addr) && quad(a.op[0].addr) && ((uintptr_t)a.out & 15) == 0 && ((uintptr_t)a.op[0].ptr & 15) == 0) {
+            const int inner4 = inner / 4;
+            int lg = 3;
+            while (lg < 8 && (1 << lg) < inner4) lg++;
+            const int TX = 1 << lg, TY = 256 >> lg;
+            const int64_t row_blocks = ((int64_t)a.n_rows + TY - 1) / TY;
+            int64_t gx = ((int64_t)inner4 + 4 * TX - 1) / (4 * TX);
+            if (gx * row_blocks < 4 * (int64_t)device_sms()) gx = ((int64_t)inner4 + TX - 1) / TX;
+            dim3 grid((unsigned)gx, (unsigned)std::min<int64_t>(row_blocks, 65535));
+            if (a.er[2] == 2) nest_pool_kernel<2><<<grid, 256, 0, s>>>(a, lg);
+            else nest_pool_kernel<4><<<grid, 256, 0, s>>>(a, lg);
+            return 4;
         }
     }
     int tx_log2 = 3;

@@ -16,8 +16,12 @@
 //    operand count, on whether any guard exists and on whether there is a
 //    reduction, so reduction-free unguarded nests (broadcast_add) compile to
 //    load / op / store.
-//  * nest_vec4_kernel: reduction-free unguarded nests with 16-byte aligned
-//    contiguous rows (elementwise / broadcast): float4 loads and stores.
+//  * nest_vec4_kernel: reduction-free nests with 16-byte aligned contiguous
+//    rows (elementwise / broadcast / concat): float4 loads and stores; a
+//    group of four points that straddles a guard boundary loads by element.
+//  * nest_pool_kernel: non-overlapping pooling along the innermost dim (window
+//    == stride, contiguous): the window's inputs of four outputs are one
+//    contiguous run, read as float4s.
 //  * nest_transpose_kernel: a reduction-free single-operand nest whose operand
 //    is contiguous along another output dim than the output is (transpose,
 //    any permutation) goes through 32 x 32 shared-memory tiles so both sides
@@ -167,10 +171,10 @@ __global__ void __launch_bounds__(256) nest_rows_kernel(const NestFastArgs p, in
     }
 }
 
-// Reduction-free, unguarded nests whose operands are contiguous (or constant)
-// along the innermost output dim, 16-byte aligned rows: four float4 groups per
+// Reduction-free nests whose operands are contiguous (or constant) along the
+// innermost output dim, 16-byte aligned rows, guarded or not: four float4 groups per
 // thread per trip (64 B per operand in flight per thread).  i counts float4s.
-template <int NOPS>
+template <int NOPS, bool GUARDS>
 __global__ void __launch_bounds__(256) nest_vec4_kernel(const NestFastArgs p, int tx_log2) {
     const int TX = 1 << tx_log2, TY = 256 >> tx_log2;
     const int tx = threadIdx.x & (TX - 1), ty = threadIdx.x >> tx_log2;
@@ -180,8 +184,14 @@ __global__ void __launch_bounds__(256) nest_vec4_kernel(const NestFastArgs p, in
         const int p2 = row % p.eo[2], r1 = row / p.eo[2];
         const int p1 = r1 % p.eo[1], p0 = r1 / p.eo[1];
         const float *src[NOPS];
+        int gb[NOPS][kNfGuards];
 #pragma unroll
-        for (int o = 0; o < NOPS; o++) src[o] = p.op[o].ptr + p.op[o].addr.base + nf_dot3(p.op[o].addr.co, p0, p1, p2);
+        for (int o = 0; o < NOPS; o++) {
+            src[o] = p.op[o].ptr + p.op[o].addr.base + nf_dot3(p.op[o].addr.co, p0, p1, p2);
+#pragma unroll
+            for (int q = 0; q < kNfGuards; q++)
+                gb[o][q] = GUARDS ? p.op[o].guard[q].base + nf_dot3(p.op[o].guard[q].co, p0, p1, p2) : 0;
+        }
         float *dst = p.out + p.out_addr.base + nf_dot3(p.out_addr.co, p0, p1, p2);
         for (int i0 = blockIdx.x * TX + tx; i0 < inner4; i0 += 4 * stride) {
             float4 v[NOPS][4];
@@ -191,11 +201,35 @@ __global__ void __launch_bounds__(256) nest_vec4_kernel(const NestFastArgs p, in
                 if (i < inner4) {
 #pragma unroll
                     for (int o = 0; o < NOPS; o++) {
-                        if (p.op[o].addr.co[3]) {
-                            v[o][u] = __ldg(reinterpret_cast<const float4 *>(src[o]) + i);
+                        const NfOperand &od = p.op[o];
+                        bool ok[4] = {true, true, true, true};
+                        if (GUARDS) {
+                            // a group of four points is all inside its guards (vector load), all
+                            // outside (the fill) or straddles a boundary (element by element)
+#pragma unroll
+                            for (int q = 0; q < kNfGuards; q++)
+                                if (q < od.n_guards) {
+#pragma unroll
+                                    for (int e = 0; e < 4; e++)
+                                        ok[e] = ok[e] && (unsigned)(gb[o][q] + od.guard[q].co[3] * (4 * i + e)) < od.guard_size[q];
+                                }
+                        }
+                        const bool all = ok[0] && ok[1] && ok[2] && ok[3], any = ok[0] || ok[1] || ok[2] || ok[3];
+                        if (!any) {
+                            v[o][u] = make_float4(od.fill, od.fill, od.fill, od.fill);
+                        } else if (od.addr.co[3]) {
+                            if (all) {
+                                v[o][u] = __ldg(reinterpret_cast<const float4 *>(src[o]) + i);
+                            } else {
+                                v[o][u].x = ok[0] ? __ldg(src[o] + 4 * i) : od.fill;
+                                v[o][u].y = ok[1] ? __ldg(src[o] + 4 * i + 1) : od.fill;
+                                v[o][u].z = ok[2] ? __ldg(src[o] + 4 * i + 2) : od.fill;
+                                v[o][u].w = ok[3] ? __ldg(src[o] + 4 * i + 3) : od.fill;
+                            }
                         } else {
                             const float b = __ldg(src[o]);
-                            v[o][u] = make_float4(b, b, b, b);
+                            v[o][u] = make_float4(ok[0] ? b : od.fill, ok[1] ? b : od.fill, ok[2] ? b : od.fill,
+                                                  ok[3] ? b : od.fill);
                         }
                     }
                 }
@@ -219,6 +253,69 @@ __global__ void __launch_bounds__(256) nest_vec4_kernel(const NestFastArgs p, in
                     }
                     reinterpret_cast<float4 *>(dst)[i] = t;
                 }
+            }
+        }
+    }
+}
+
+// Non-overlapping pooling along the innermost dim: one operand, no guards, the
+// innermost reduction dim contiguous with extent E equal to the operand's
+// stride along the innermost output dim (window == stride), 16-byte aligned
+// rows.  A thread owns groups of four consecutive outputs: per outer reduction
+// step their 4 E inputs are one contiguous run, read as E float4s, and the
+// window's terms fold in the reference order (outer reduction dims, then the
+// window).  Four groups per trip.
+template <int E>
+__global__ void __launch_bounds__(256) nest_pool_kernel(const NestFastArgs p, int tx_log2) {
+    const int TX = 1 << tx_log2, TY = 256 >> tx_log2;
+    const int tx = threadIdx.x & (TX - 1), ty = threadIdx.x >> tx_log2;
+    const int inner4 = p.eo[3] >> 2;
+    const int stride = gridDim.x * TX;
+    const NfOperand &od = p.op[0];
+    const float id = identity_rt(p.reduce);
+    for (int row = blockIdx.y * TY + ty; row < p.n_rows; row += gridDim.y * TY) {
+        const int p2 = row % p.eo[2], r1 = row / p.eo[2];
+        const int p1 = r1 % p.eo[1], p0 = r1 / p.eo[1];
+        const float *src = od.ptr + od.addr.base + nf_dot3(od.addr.co, p0, p1, p2);
+        float *dst = p.out + p.out_addr.base + nf_dot3(p.out_addr.co, p0, p1, p2);
+        for (int i0 = blockIdx.x * TX + tx; i0 < inner4; i0 += 4 * stride) {
+            float acc[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) acc[u][j] = id;
+            for (int d0 = 0; d0 < p.er[0]; d0++)
+                for (int d1 = 0; d1 < p.er[1]; d1++) {
+                    const float4 *line = reinterpret_cast<const float4 *>(src + od.addr.cr[0] * d0 + od.addr.cr[1] * d1);
+                    float4 w[4][E];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int i = i0 + u * stride;
+                        if (i < inner4) {
+#pragma unroll
+                            for (int e = 0; e < E; e++) w[u][e] = __ldg(line + i * E + e);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        if (i0 + u * stride < inner4) {
+#pragma unroll
+                            for (int j = 0; j < 4; j++)
+#pragma unroll
+                                for (int d2 = 0; d2 < E; d2++) {
+                                    const int f = j * E + d2;   // float f of the run: float4 f / 4, lane f % 4
+                                    const float4 q = w[u][f >> 2];
+                                    float t = (f & 3) == 0 ? q.x : (f & 3) == 1 ? q.y : (f & 3) == 2 ? q.z : q.w;
+                                    if (p.beta != 1.0f) t = __fmul_rn(p.beta, t);
+                                    acc[u][j] = op_rt(p.reduce, acc[u][j], t);
+                                }
+                        }
+                    }
+                }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int i = i0 + u * stride;
+                if (i < inner4) reinterpret_cast<float4 *>(dst)[i] = make_float4(acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
             }
         }
     }

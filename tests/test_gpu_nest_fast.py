@@ -60,15 +60,26 @@ def _graph(name, sizes):
     g = json.loads(common.graph_json(case["graph"]))
     for var, n in sizes.items():
         g = shard.shard_graph(g, n, var)
+    if name == "acc_concat":
+        # the second operand's view starts where the first ends (the golden
+        # graph's -3 is its own c1): keep the resized graph a concat
+        for node in g["nodes"]:
+            for c in node.get("constraints", []):
+                if c["offset"] == -3:
+                    c["offset"] = -sizes["c1"]
     return json.dumps(g)
 
 
 RESIZED = [
     ("acc_maxpool", {"h": 260, "w": 1002, "r": 130, "c": 501}, 1),
     ("acc_maxpool", {"h": 64, "w": 12, "r": 32, "c": 6}, 1),
+    ("acc_maxpool", {"h": 70, "w": 1000, "r": 35, "c": 500}, 4),
+    ("acc_maxpool", {"h": 6, "w": 40, "r": 3, "c": 20}, 4),
     ("acc_transpose", {"a": 300, "b": 517, "r": 517, "c": 300}, 2),
     ("acc_transpose", {"a": 33, "b": 8, "r": 8, "c": 33}, None),
     ("acc_concat", {"r": 129, "c1": 200, "c2": 333, "c": 533}, 1),
+    ("acc_concat", {"r": 129, "c1": 200, "c2": 332, "c": 532}, 3),
+    ("acc_concat", {"r": 33, "c1": 202, "c2": 334, "c": 536}, None),
     ("acc_broadcast_add", {"m": 257, "n": 1030}, 1),
     ("acc_broadcast_add", {"m": 257, "n": 1032}, 3),
     ("acc_broadcast_add", {"m": 9, "n": 4096}, 3),

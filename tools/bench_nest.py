@@ -28,6 +28,11 @@ def graph(name, sizes):
     g = json.loads(common.graph_json(case["graph"]))
     for var, n in sizes.items():
         g = shard.shard_graph(g, n, var)
+    if name == "acc_concat":   # the second view starts where the first ends (the golden graph's -3 is its c1)
+        for node in g["nodes"]:
+            for c in node.get("constraints", []):
+                if c["offset"] == -3:
+                    c["offset"] = -sizes["c1"]
     return json.dumps(g)
 
 
