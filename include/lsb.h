@@ -269,7 +269,7 @@ int lsb_conv2d_nchw(const lsb_conv_desc *desc, void *stream);
 int lsb_affine_nest(const lsb_nest_desc *desc, void *stream);
 /* diagnostics: which kernel the last lsb_affine_nest call launched --
  * 0 affine_nest_kernel (general), 1 nest_rows_kernel, 2 nest_transpose_kernel,
- * 3 nest_vec4_kernel, 4 nest_pool_kernel */
+ * 3 nest_vec4_kernel, 4 nest_pool_kernel, 5 nest_transpose4_kernel */
 int lsb_last_nest_kernel(int *kind);
 
 /* per-kernel timing for rooflines: when enabled, the dominant kernel of each

@@ -83,6 +83,18 @@ int launch_nest_fast(const lsb_nest_desc &d, const EpiStages &epi, cudaStream_t 
             a.tb0 = q == 0 ? 1 : 0;
             a.tb1 = q == 2 ? 1 : 2;
             const int64_t batch = (int64_t)a.eo[a.tb0] * a.eo[a.tb1];
+            // both sides in whole float4s: 64 x 64 tiles
+            const NfAffine &fi = a.op[0].addr, &fo = a.out_addr;
+            const bool v4 = inner % 4 == 0 && a.eo[q] % 4 == 0 && fi.base % 4 == 0 && fi.co[3] % 4 == 0 &&
+                            fi.co[a.tb0] % 4 == 0 && fi.co[a.tb1] % 4 == 0 && fo.base % 4 == 0 && fo.co[q] % 4 == 0 &&
+                            fo.co[a.tb0] % 4 == 0 && fo.co[a.tb1] % 4 == 0 && ((uintptr_t)a.out & 15) == 0 &&
+                            ((uintptr_t)a.op[0].ptr & 15) == 0;
+            if (v4 && (a.eo[q] + 63) / 64 <= 65535) {
+                dim3 g4((unsigned)((inner + 63) / 64), (unsigned)((a.eo[q] + 63) / 64),
+                        (unsigned)std::min<int64_t>(batch, 65535));
+                nest_transpose4_kernel<<<g4, 256, 0, s>>>(a);
+                return 5;
+            }
             dim3 grid((unsigned)((inner + kNfTileI - 1) / kNfTileI), (unsigned)((a.eo[q] + kNfTileQ - 1) / kNfTileQ),
                       (unsigned)std::min<int64_t>(batch, 65535));
             if (grid.y <= 65535) {

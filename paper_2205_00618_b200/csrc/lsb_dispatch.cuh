@@ -42,7 +42,7 @@ void prof_mark(int which, cudaStream_t s);
 
 // the 32-bit row-walking / tiled-transpose nest kernels (nest_fast.cuh):
 // returns 0 when the nest does not qualify (caller runs affine_nest_kernel),
-// 1 = nest_rows_kernel, 2 = nest_transpose_kernel, 3 = nest_vec4_kernel, 4 = nest_pool_kernel launched
+// 1 = nest_rows_kernel, 2 = nest_transpose_kernel, 3 = nest_vec4_kernel, 4 = nest_pool_kernel, 5 = nest_transpose4_kernel launched
 int launch_nest_fast(const lsb_nest_desc &d, const EpiStages &epi, cudaStream_t s);
 
 GemmFn fast_gemm(int combine, int reduce, int bm, bool two_level);   // kern_fast.cu (nullptr if untuned)

@@ -317,7 +317,7 @@ def last_gemm_launch() -> dict:
 
 
 def last_nest_kernel() -> int:
-    """Which kernel the last affine-nest call launched: 0 general, 1 rows, 2 transpose, 3 vec4, 4 pool."""
+    """Which kernel the last affine-nest call launched: 0 general, 1 rows, 2 transpose, 3 vec4, 4 pool, 5 transpose4."""
     k = ctypes.c_int(0)
     check(lib().lsb_last_nest_kernel(ctypes.byref(k)), "lsb_last_nest_kernel")
     return k.value

@@ -77,6 +77,8 @@ RESIZED = [
     ("acc_maxpool", {"h": 6, "w": 40, "r": 3, "c": 20}, 4),
     ("acc_transpose", {"a": 300, "b": 517, "r": 517, "c": 300}, 2),
     ("acc_transpose", {"a": 33, "b": 8, "r": 8, "c": 33}, None),
+    ("acc_transpose", {"a": 300, "b": 516, "r": 516, "c": 300}, 5),
+    ("acc_transpose", {"a": 64, "b": 128, "r": 128, "c": 64}, 5),
     ("acc_concat", {"r": 129, "c1": 200, "c2": 333, "c": 533}, 1),
     ("acc_concat", {"r": 129, "c1": 200, "c2": 332, "c": 532}, 3),
     ("acc_concat", {"r": 33, "c1": 202, "c2": 334, "c": 536}, None),
