@@ -155,7 +155,9 @@ static int duo_ctas(int64_t units) {
     }
     return (int)std::min<int64_t>(units, (int64_t)occ * device_sms());
 }
-int maxplus_duo_ctas(int64_t units, int bk) { return bk == 8 ? duo_ctas<8>(units) : duo_ctas<16>(units); }
+int maxplus_duo_ctas(int64_t units, int bk) {
+    return bk == 8 ? duo_ctas<8>(units) : bk == 32 ? duo_ctas<32>(units) : duo_ctas<16>(units);
+}
 
 template <int BK>
 static int launch_duo(int reduce, const GemmArgs &a, int ctas, float4 *part, int *flags, int epoch, cudaStream_t s) {
@@ -176,8 +178,9 @@ static int launch_duo(int reduce, const GemmArgs &a, int ctas, float4 *part, int
 }
 int launch_maxplus_duo(int reduce, const GemmArgs &a, int bk, int ctas, float4 *part, int *flags, int epoch,
                        cudaStream_t s) {
-    return bk == 8 ? launch_duo<8>(reduce, a, ctas, part, flags, epoch, s)
-                   : launch_duo<16>(reduce, a, ctas, part, flags, epoch, s);
+    return bk == 8    ? launch_duo<8>(reduce, a, ctas, part, flags, epoch, s)
+           : bk == 32 ? launch_duo<32>(reduce, a, ctas, part, flags, epoch, s)
+                      : launch_duo<16>(reduce, a, ctas, part, flags, epoch, s);
 }
 
 void launch_conv_fold(const ConvArgs &a, int64_t n_img, cudaStream_t s) {

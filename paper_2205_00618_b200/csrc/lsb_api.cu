@@ -95,7 +95,7 @@ void read_knobs(lsb::Knobs &k) {
     if (const char *e = getenv("LSB_MP_MODE")) k.mp_mode = !strcmp(e, "cluster") ? 1 : !strcmp(e, "streamk") ? 2 : !strcmp(e, "fixup") ? 3 : 0;
     k.fixup_ctas = num("LSB_FIXUP_CTAS");
     k.tc_chunk_k = num("LSB_TC_CHUNK_K");
-    k.duo_bk = num("LSB_DUO_BK") == 8 ? 8 : 16;
+    k.duo_bk = num("LSB_DUO_BK") == 8 ? 8 : num("LSB_DUO_BK") == 16 ? 16 : 32;
     k.mp_cluster = num("LSB_MP_CLUSTER");
     k.streamk_ctas = num("LSB_STREAMK_CTAS");
     k.conv_splits = num("LSB_CONV_SPLITS");
@@ -573,7 +573,7 @@ int lsb_semiring_gemm(const lsb_gemm_desc *d, void *stream) {
             if (fast && mode == 0) {
                 // one 512-thread CTA per SM, two groups sharing each segment's
                 // slices dynamically (C2: 0.078 -> see DESIGN 3.2b)
-                const int bk = lsb::knobs().duo_bk;
+                const int bk = (lsb::knobs().duo_bk == 32 && d->K % 32) ? 16 : lsb::knobs().duo_bk;
                 const int64_t units = t128 * (d->K / bk);
                 int ctas = lsb::maxplus_duo_ctas(units, bk);
                 if (lsb::knobs().fixup_ctas > 0) ctas = std::max(1, std::min(ctas, lsb::knobs().fixup_ctas));

@@ -388,7 +388,10 @@ struct DuoCfg {
     static constexpr int kApitch = BK + 4;
     static constexpr int kStageFloats = kMpBM * kApitch + BK * kMpBN;
     static constexpr int kRingFloats = kStages * kStageFloats;
-    static constexpr size_t kSmemBytes = sizeof(float) * (2 * kRingFloats) + sizeof(float4) * 16 * kThreads;
+    // the accumulator exchange of a segment's end reuses the rings (each group sends
+    // into its own, free by then: 8 float4 slots x 256 threads = 32 KB)
+    static constexpr size_t kSmemBytes = sizeof(float) * (2 * kRingFloats);
+    static_assert(sizeof(float) * kRingFloats >= sizeof(float4) * 8 * kThreads, "ring holds the exchange");
 };
 
 __device__ __forceinline__ void mp_group_bar(int g) { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); }
@@ -402,28 +405,24 @@ __device__ __forceinline__ void mp_group_slices(const GemmArgs &p, float *ring, 
     using Cf = DuoCfg<BK>;
     constexpr int S = Cf::kStages, kPer = BK / 8;   // 16-B chunks per thread and operand
     const int t = threadIdx.x & (kThreads - 1), tx = t & 15, ty = t >> 4;
-    // chunk j of this thread: A row (t + 256 j) / (BK / 4), k quad (t + 256 j) % (BK / 4);
-    // B k row (t + 256 j) >> 5, column quad t & 31
-    const float *ga[kPer], *gb[kPer];
-    int sa[kPer], sb[kPer];
-#pragma unroll
-    for (int j = 0; j < kPer; j++) {
-        const int c = t + j * kThreads;
-        const int a_row = c / (BK / 4), a_kq = (c % (BK / 4)) * 4;
-        const int b_k = c >> 5, b_nq = (c & 31) * 4;
-        ga[j] = p.A + min(m0 + a_row, p.M - 1) * p.sa_m + k0 + a_kq;
-        gb[j] = p.B + (k0 + b_k) * p.sb_k + min(n0 + b_nq, p.N - 4);
-        sa[j] = a_row * Cf::kApitch + a_kq;
-        sb[j] = kMpBM * Cf::kApitch + b_k * kMpBN + b_nq;
-    }
+    // 16-B chunk j of this thread: A row t / (BK / 4) + j * (1024 / BK), k quad t % (BK / 4);
+    // B k row (t >> 5) + 8 j, column quad t & 31.  Addresses are rebuilt per
+    // issue from two base pointers (per-chunk pointers spill at BK = 32).
+    constexpr int kQuads = BK / 4, kRowsPerPass = kThreads / kQuads;
+    const int a_row0 = t / kQuads, a_kq = (t % kQuads) * 4;
+    const int b_k0 = t >> 5, b_nq = (t & 31) * 4;
+    const float *ga = p.A + k0 + a_kq;
+    const float *gb = p.B + (k0 + b_k0) * p.sb_k + min(n0 + b_nq, p.N - 4);
     const int64_t b_step = BK * p.sb_k;
 
     auto issue = [&](int slice, int stage) {
         float *st = ring + stage * Cf::kStageFloats;
 #pragma unroll
         for (int j = 0; j < kPer; j++) {
-            cp_async16(st + sa[j], ga[j] + slice * BK);
-            cp_async16(st + sb[j], gb[j] + slice * b_step);
+            const int a_row = a_row0 + j * kRowsPerPass;
+            cp_async16(st + a_row * Cf::kApitch + a_kq, ga + min(m0 + a_row, p.M - 1) * p.sa_m + slice * BK);
+            cp_async16(st + kMpBM * Cf::kApitch + (b_k0 + 8 * j) * kMpBN + b_nq,
+                       gb + slice * b_step + (int64_t)(8 * j) * p.sb_k);
         }
     };
 
@@ -495,7 +494,7 @@ struct MpDuoTail {
         for (int i = 0; i < 4; i++)
 #pragma unroll
             for (int h = 0; h < 2; h++)
-                xch[(GI * 8 + i * 2 + h) * kThreads + t] = make_float4(acc[kOther + i][2 * h].x, acc[kOther + i][2 * h].y,
+                xch[(i * 2 + h) * kThreads + t] = make_float4(acc[kOther + i][2 * h].x, acc[kOther + i][2 * h].y,
                                                                        acc[kOther + i][2 * h + 1].x, acc[kOther + i][2 * h + 1].y);
     }
     static __device__ __forceinline__ void fold4(float2 (&acc)[8][4], int i, int h, const float4 w) {
@@ -509,7 +508,7 @@ struct MpDuoTail {
 #pragma unroll
         for (int i = 0; i < 4; i++)
 #pragma unroll
-            for (int h = 0; h < 2; h++) fold4(acc, i, h, xch[((1 - GI) * 8 + i * 2 + h) * kThreads + t]);
+            for (int h = 0; h < 2; h++) fold4(acc, i, h, xch[(i * 2 + h) * kThreads + t]);
     }
     // partial tile slots of this group: (kOwn + i) * 2 + h
     static __device__ __forceinline__ void publish(float4 *dst, int t, const float2 (&acc)[8][4]) {
@@ -582,7 +581,9 @@ __global__ void __launch_bounds__(kDuoThreads, 1) maxplus_duo_kernel(const GemmA
     __shared__ int s_q[2][Cf::kStages];
     const int g = threadIdx.x >> 8, t = threadIdx.x & (kThreads - 1), tx = t & 15, ty = t >> 4;
     float *ring = mp_smem + g * Cf::kRingFloats;
-    float4 *xch = reinterpret_cast<float4 *>(mp_smem + 2 * Cf::kRingFloats);
+    // exchange areas: a group sends into its own ring and receives from the other's
+    float4 *xch_mine = reinterpret_cast<float4 *>(ring);
+    const float4 *xch_other = reinterpret_cast<const float4 *>(mp_smem + (1 - g) * Cf::kRingFloats);
     const int64_t n_tiles = (p.N + kMpBN - 1) / kMpBN, m_tiles = (p.M + kMpBM - 1) / kMpBM;
     const int64_t ks = p.K / BK;
     const int64_t U = m_tiles * n_tiles * ks, G = gridDim.x, b = blockIdx.x;
@@ -617,11 +618,11 @@ __global__ void __launch_bounds__(kDuoThreads, 1) maxplus_duo_kernel(const GemmA
         mp_acc_init<OPR>(acc);
         mp_group_slices<OPR, BK>(p, ring, m0, n0, s0 * BK, (int)(seg_end - u), acc, &s_next, s_q[g], g);
         MP_STAMP(2);   // group 0's slices done
-        if (g == 0) MpDuoTail<OPR, 0>::send(xch, t, acc);
-        else MpDuoTail<OPR, 1>::send(xch, t, acc);
+        if (g == 0) MpDuoTail<OPR, 0>::send(xch_mine, t, acc);
+        else MpDuoTail<OPR, 1>::send(xch_mine, t, acc);
         __syncthreads();
-        if (g == 0) MpDuoTail<OPR, 0>::recv(xch, t, acc);
-        else MpDuoTail<OPR, 1>::recv(xch, t, acc);
+        if (g == 0) MpDuoTail<OPR, 0>::recv(xch_other, t, acc);
+        else MpDuoTail<OPR, 1>::recv(xch_other, t, acc);
         MP_STAMP(6);   // halves merged
         if (s0 != 0) {
             // contributor: this CTA's (only) partial tile, thread-major float4s

@@ -259,13 +259,13 @@ def test_tropical_split_k_paths(op, shape):
     _same(got[out].reshape(m, n)[rows], ref[out], exact=True)
 
 
-@pytest.mark.parametrize("mode", ["duo", "duo:8", "fixup", "cluster", "streamk"])
+@pytest.mark.parametrize("mode", ["duo", "duo:8", "duo:16", "fixup", "cluster", "streamk"])
 @pytest.mark.parametrize("op,shape", [("add_max", (1024, 1024, 1024)), ("add_min", (777, 1040, 1000)),
                                       ("add_max", (130, 4096, 260)), ("add_min", (2048, 512, 1100))])
 def test_tropical_underfilled_modes(mode, op, shape, monkeypatch):
     """The kernels for underfilled (add, max|min) grids -- stream-K with the
     in-kernel fixup as one 512-thread CTA per SM whose two groups pull slices
-    from a shared counter (duo, the default; 16- or 8-deep slices) or as two
+    from a shared counter (duo, the default; 32-, 16- or 8-deep slices) or as two
     CTAs per SM (fixup), cluster split-K with DSMEM folds, stream-K with
     atomic merges (LSB_MP_MODE) -- give the same bytes as the reference, NaN /
     inf included, wherever the partial boundaries fall."""
