@@ -203,18 +203,34 @@ __global__ void __launch_bounds__(256) nest_vec4_kernel(const NestFastArgs p, in
                     for (int o = 0; o < NOPS; o++) {
                         const NfOperand &od = p.op[o];
                         bool ok[4] = {true, true, true, true};
+                        bool all = true, any = true;
                         if (GUARDS) {
                             // a group of four points is all inside its guards (vector load), all
-                            // outside (the fill) or straddles a boundary (element by element)
+                            // outside (the fill) or straddles a boundary (element by element).
+                            // A guard is an interval of an affine form, so the ends decide "all";
+                            // the middle points are only evaluated when the ends disagree or are
+                            // both outside (a window narrower than the group).
+                            bool first = true, last = true;
 #pragma unroll
                             for (int q = 0; q < kNfGuards; q++)
                                 if (q < od.n_guards) {
-#pragma unroll
-                                    for (int e = 0; e < 4; e++)
-                                        ok[e] = ok[e] && (unsigned)(gb[o][q] + od.guard[q].co[3] * (4 * i + e)) < od.guard_size[q];
+                                    const int g0 = gb[o][q] + od.guard[q].co[3] * (4 * i);
+                                    first = first && (unsigned)g0 < od.guard_size[q];
+                                    last = last && (unsigned)(g0 + 3 * od.guard[q].co[3]) < od.guard_size[q];
                                 }
+                            all = first && last;
+                            if (!all) {
+                                ok[0] = first;
+                                ok[3] = last;
+#pragma unroll
+                                for (int e = 1; e < 3; e++)
+#pragma unroll
+                                    for (int q = 0; q < kNfGuards; q++)
+                                        if (q < od.n_guards)
+                                            ok[e] = ok[e] && (unsigned)(gb[o][q] + od.guard[q].co[3] * (4 * i + e)) < od.guard_size[q];
+                                any = ok[0] || ok[1] || ok[2] || ok[3];
+                            }
                         }
-                        const bool all = ok[0] && ok[1] && ok[2] && ok[3], any = ok[0] || ok[1] || ok[2] || ok[3];
                         if (!any) {
                             v[o][u] = make_float4(od.fill, od.fill, od.fill, od.fill);
                         } else if (od.addr.co[3]) {
