@@ -237,8 +237,10 @@ def test_c4_alpha_form():
 def test_c5_gemm_16384_full():
     """Every one of the 16384^2 outputs against an f64 GEMM (computed on the
     device in torch float64 -- the f64 restatement of reference_eval's
-    (mul, add) contraction).  Gate: the reference metric
-    max|d|/max(|ref|,1) <= 1e-4; the strict per-element pass fraction is
+    (mul, add) contraction).  Gate: the reference metric, per
+    element as the reference computes it, max(|d|/max(|ref|,1)) <= 1e-4
+    (measured 8.5e-5 over all 268M outputs; the VM's own is 3.2e-4 on rows
+    0-7); the strict per-element pass fraction is
     recorded next to the reference VM's own on rows 0-7 (the VM fails the
     strict rule on ~0.6 % at K = 16384) and must not be worse than it."""
     import json
@@ -254,25 +256,29 @@ def test_c5_gemm_16384_full():
     A = torch.from_numpy(bufs[0]).to(dev).double()
     B = torch.from_numpy(bufs[1]).to(dev).double()
     Cg = torch.from_numpy(C).to(dev)
-    worst, npass, amax, tot = 0.0, 0, 0.0, 0
+    worst, npass, amax, tot, elem = 0.0, 0, 0.0, 0, 0.0
     for r in range(0, 16384, 2048):
         ref = A[r:r + 2048] @ B
         dd = (Cg[r:r + 2048].double() - ref).abs()
         worst = max(worst, float(dd.max()))
         amax = max(amax, float(ref.abs().max()))
+        # the reference's acceptance formula, per element (test_acceptance.py:57-58)
+        elem = max(elem, float((dd / ref.abs().clamp(min=1.0)).max()))
         npass += int((dd <= 1e-5 + 1e-4 * ref.abs()).sum())
         tot += ref.numel()
     metric = worst / max(amax, 1.0)
     strict = npass / tot
-    rec = {"config": "C5", "elements": tot, "ref_metric": metric, "strict_pass": strict,
+    rec = {"config": "C5", "elements": tot, "ref_metric": elem, "max_err_rel_max_ref": metric,
+           "strict_pass": strict,
            "vm_strict_pass_rows0_8": vm, "ours_strict_pass_rows0_8": float(common.strict_ok(C[:8], ref8).mean()),
-           "ours_ref_metric_rows0_8": common.ref_metric(C[:8], ref8)}
+           "ours_ref_metric_rows0_8": common.ref_metric(C[:8], ref8),
+           "vm_ref_metric_rows0_8": common.ref_metric(d["vm_rows0_8"], ref8)}
     print("C5 parity:", json.dumps(rec))
     out = os.environ.get("LSB_PARITY_OUT")
     if out:
         with open(out, "w") as f:
             json.dump(rec, f, indent=1)
-    assert metric <= 1e-4
+    assert elem <= 1e-4, rec
     assert strict >= vm, rec
 
 
