@@ -126,7 +126,7 @@ __device__ __forceinline__ void nf_strip(const NestFastArgs &p, const int (&ab)[
 
 // grid: x over the innermost dim (TX * U points per CTA trip), y over rows
 template <int NOPS, bool GUARDS, bool RED>
-__global__ void __launch_bounds__(256) nest_rows_kernel(const NestFastArgs p, int tx_log2) {
+__global__ void __launch_bounds__(256, 6) nest_rows_kernel(const NestFastArgs p, int tx_log2) {
     constexpr int U = RED ? 4 : 8;
     const int TX = 1 << tx_log2, TY = 256 >> tx_log2;
     const int tx = threadIdx.x & (TX - 1), ty = threadIdx.x >> tx_log2;
