@@ -121,11 +121,11 @@ int launch_nest_fast(const lsb_nest_desc &d, const EpiStages &epi, cudaStream_t 
             if (gx * row_blocks < 4 * (int64_t)device_sms()) gx = ((int64_t)inner4 + TX - 1) / TX;
             dim3 grid((unsigned)gx, (unsigned)std::min<int64_t>(row_blocks, 65535));
             if (d.n_operands == 1) {
-                if (guards) nest_vec4_kernel<1, true><<<grid, 256, 0, s>>>(a, lg);
-                else nest_vec4_kernel<1, false><<<grid, 256, 0, s>>>(a, lg);
+                if (guards) nest_vec4_guarded_kernel<1><<<grid, 256, 0, s>>>(a, lg);
+                else nest_vec4_kernel<1><<<grid, 256, 0, s>>>(a, lg);
             } else {
-                if (guards) nest_vec4_kernel<2, true><<<grid, 256, 0, s>>>(a, lg);
-                else nest_vec4_kernel<2, false><<<grid, 256, 0, s>>>(a, lg);
+                if (guards) nest_vec4_guarded_kernel<2><<<grid, 256, 0, s>>>(a, lg);
+                else nest_vec4_kernel<2><<<grid, 256, 0, s>>>(a, lg);
             }
             return 3;
         }

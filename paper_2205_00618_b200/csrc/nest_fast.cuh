@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(256, 6) nest_rows_kernel(const NestFastArgs p,
 // innermost output dim, 16-byte aligned rows, guarded or not: four float4 groups per
 // thread per trip (64 B per operand in flight per thread).  i counts float4s.
 template <int NOPS, bool GUARDS>
-__global__ void __launch_bounds__(256) nest_vec4_kernel(const NestFastArgs p, int tx_log2) {
+__device__ __forceinline__ void nest_vec4_body(const NestFastArgs &p, int tx_log2) {
     const int TX = 1 << tx_log2, TY = 256 >> tx_log2;
     const int tx = threadIdx.x & (TX - 1), ty = threadIdx.x >> tx_log2;
     const int inner4 = p.eo[3] >> 2;
@@ -272,6 +272,18 @@ __global__ void __launch_bounds__(256) nest_vec4_kernel(const NestFastArgs p, in
             }
         }
     }
+}
+
+// Two entry points: the unguarded body fits 48 registers (5 CTAs per SM:
+// broadcast_add 5432 -> 5580 GB/s); the guarded one is fastest at the
+// compiler's own 58 (capped to 48 or pushed to 64+ it lost 8-19 % on concat).
+template <int NOPS>
+__global__ void __launch_bounds__(256, 5) nest_vec4_kernel(const NestFastArgs p, int tx_log2) {
+    nest_vec4_body<NOPS, false>(p, tx_log2);
+}
+template <int NOPS>
+__global__ void __launch_bounds__(256) nest_vec4_guarded_kernel(const NestFastArgs p, int tx_log2) {
+    nest_vec4_body<NOPS, true>(p, tx_log2);
 }
 
 // Non-overlapping pooling along the innermost dim: one operand, no guards, the
